@@ -1,0 +1,142 @@
+// evo_kernels.cuh — argument blocks and launchers shared by the kernels and the C-ABI layer.
+#pragma once
+#include "evo_common.cuh"
+
+namespace evo {
+
+constexpr int kMaxMaskWords = 512;  // Lk <= 16384
+constexpr int kMaxLk = kMaxMaskWords * 32;
+
+// ------------------------------------------------------------------ forward (bf16, tcgen05)
+struct FwdArgs {
+  int B, H, Lq, Lk, D;
+  float scale_log2;  // scale * log2(e)
+  int bias_batched;  // per-batch bias: TMA coordinate 3 = b
+  const uint8_t* mask;
+  int64_t mask_s0, mask_s1;
+  const __nv_bfloat16* g;
+  int64_t g_sb, g_sh, g_sl;
+  __nv_bfloat16* o;
+  int64_t o_sb, o_sh, o_sl;
+  float* lse;
+};
+struct FwdLaunch {
+  CUtensorMap tm_q, tm_k, tm_v, tm_b;
+  FwdArgs args;
+};
+inline size_t fwd_smem_bytes(int DP) {
+  return 5 * 128 * (size_t)DP * 2 + 65536 + kMaxMaskWords * 4 + 2 * 256 * 4 + 8 * 8 + 16;
+}
+cudaError_t launch_fwd_bf16(const FwdLaunch& L, int DP, int bias_mode, cudaStream_t st);
+
+// ------------------------------------------------------------------ backward (bf16)
+struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
+  int B, H, Lq, D;
+  const void* o;  // bf16 or f32 (dtype)
+  const void* dout;
+  int64_t o_sb, o_sh, o_sl;  // also dout strides
+  const void* g;
+  int64_t g_sb, g_sh, g_sl;  // also dg strides
+  void* dg;
+  const float* lse;
+  float* lse2;   // lse*log2e, +inf for rows with no kept key (bf16 path) | lse (f32 path)
+  float* Dvec;   // Σ_d dO·o
+  void* dA;      // [B,H,Lq,D] contiguous dO·sigmoid(g) (NULL when no gate)
+};
+cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st);
+
+struct BwdMainArgs {  // dK, dV (and dQ partials) — CTA per (b, h, key tile)
+  int B, H, Lq, Lk, D;
+  float scale, scale_log2;
+  int bias_batched;
+  const uint8_t* mask;
+  int64_t mask_s0, mask_s1;
+  const float* lse2;
+  const float* Dvec;
+  __nv_bfloat16* dk;
+  int64_t k_sb, k_sh, k_sl;
+  __nv_bfloat16* dv;
+  int64_t v_sb, v_sh, v_sl;
+  __nv_bfloat16* dq;  // direct store when there is a single key tile
+  int64_t q_sb, q_sh, q_sl;
+  float* dq_acc;      // [B,H,Lq,D] fp32 accumulator otherwise
+};
+struct BwdMainLaunch {
+  CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
+  BwdMainArgs args;
+};
+inline size_t bwd_main_smem_bytes(int DP) {
+  // Pt, dSt, bias[2] (128 KB) | K, V, Q[2], dA[2] tiles | vectors[2] (2 KB) | barriers
+  return 131072 + 6 * 128 * (size_t)DP * 2 + 2048 + 16 * 8 + 16;
+}
+cudaError_t launch_bwd_main_bf16(const BwdMainLaunch& L, int DP, int bias_mode, cudaStream_t st);
+
+struct BwdBiasArgs {  // dbias partials — CTA per (h, q tile, k tile, batch chunk)
+  int B, H, Lq, Lk, D;
+  float scale_log2;
+  int bias_batched;
+  int nchunks, chunk;  // batch rows per chunk
+  const uint8_t* mask;
+  int64_t mask_s0, mask_s1;
+  const float* lse2;
+  const float* Dvec;
+  float* partial;  // shared: [nchunks][H][Lq][Lk]; per-batch: [B][H][Lq][Lk]
+};
+struct BwdBiasLaunch {
+  CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
+  BwdBiasArgs args;
+};
+inline size_t bwd_bias_smem_bytes(int DP) {
+  // per stage: Q, K, V, dA tiles + bias tile; 2 stages; barriers
+  return 2 * (4 * 128 * (size_t)DP * 2 + 32768 + 1024) + 16 * 8 + 16;
+}
+cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, cudaStream_t st);
+
+struct ReduceArgs {  // dbias[h,q,k] (bias strides) = Σ_c partial[c][h][q][k]
+  int nparts, H, Lq, Lk;
+  int64_t nb;        // leading count of the destination (1 shared, B per-batch)
+  const float* partial;
+  float* dbias;
+  int64_t s_b, s_h, s_q, s_k;
+  int q_fast;        // destination is q-contiguous
+};
+cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st);
+
+struct ConvertArgs {  // dq = bf16(scale * dq_acc)
+  int B, H, Lq, D;
+  float scale;
+  const float* acc;
+  __nv_bfloat16* dq;
+  int64_t q_sb, q_sh, q_sl;
+};
+cudaError_t launch_dq_convert(const ConvertArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------------ fp32 verification path
+struct F32Args {
+  int B, H, Lq, Lk, D;
+  float scale;
+  const float *q, *k, *v, *g, *bias;
+  int64_t q_sb, q_sh, q_sl, k_sb, k_sh, k_sl, v_sb, v_sh, v_sl, g_sb, g_sh, g_sl;
+  int bias_kind;
+  int64_t b_sb, b_sh, b_sq, b_sk;
+  const uint8_t* mask;
+  int64_t mask_s0, mask_s1;
+  float* o;
+  int64_t o_sb, o_sh, o_sl;
+  float* lse;
+  // backward
+  const float* dout;
+  const float* dA;    // [B,H,Lq,D] contiguous, or dout (then strides = o strides)
+  int64_t a_sb, a_sh, a_sl;
+  const float* lse_in;
+  const float* Dvec;
+  float *dq, *dk, *dv, *dbias;
+};
+cudaError_t launch_fwd_f32(const F32Args& a, cudaStream_t st);
+cudaError_t launch_bwd_f32(const F32Args& a, cudaStream_t st, int* nlaunch);
+
+cudaError_t launch_fill_empty(float* lse, int64_t nrows, void* o, int dtype, int B, int H,
+                              int Lq, int D, int64_t o_sb, int64_t o_sh, int64_t o_sl,
+                              cudaStream_t st);
+
+}  // namespace evo

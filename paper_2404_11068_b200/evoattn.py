@@ -1,0 +1,245 @@
+"""Thin Python binding of the C ABI in ``include/evo_attn.h`` (argument marshalling only).
+
+Every step of the attention path runs in ``libevoattn.so`` (hand-written sm_100a kernels).
+PyTorch supplies device memory, the current CUDA stream and nothing else.  There is no CPU
+fallback: if the library is missing, or a call returns an error, this module raises.
+
+Tensor conventions (logical views; any strides, head dim unit-stride):
+  q, g, o, dout : [B, H, Lq, D]        k, v : [B, H, Lk, D]
+  bias          : [H, Lq, Lk] (shared over B) or [B, H, Lq, Lk]; q- or k-unit-stride
+  mask          : [B, Lk] uint8/bool (nonzero = keep), any strides
+  lse           : [B, H, Lq] fp32 contiguous
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libevoattn.so")
+_lock = threading.Lock()
+_lib = None
+
+EVO_BF16, EVO_F32 = 0, 1
+EVO_BIAS_NONE, EVO_BIAS_SHARED, EVO_BIAS_PER_BATCH = 0, 1, 2
+STATUS = {0: "EVO_OK", 1: "EVO_E_INVALID", 2: "EVO_E_SHAPE", 3: "EVO_E_ALIGN",
+          4: "EVO_E_UNSUPPORTED", 5: "EVO_E_WORKSPACE", 6: "EVO_E_CUDA"}
+
+
+class EvoError(RuntimeError):
+    def __init__(self, status, detail):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+
+
+class Desc(ctypes.Structure):
+    """Mirror of evo_attn_desc_t (natural C alignment, x86-64)."""
+    _fields_ = [
+        ("B", ctypes.c_int64), ("H", ctypes.c_int32), ("Lq", ctypes.c_int32),
+        ("Lk", ctypes.c_int32), ("D", ctypes.c_int32), ("dtype", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+        ("q_str", ctypes.c_int64 * 3), ("k_str", ctypes.c_int64 * 3),
+        ("v_str", ctypes.c_int64 * 3), ("g_str", ctypes.c_int64 * 3),
+        ("o_str", ctypes.c_int64 * 3),
+        ("bias_kind", ctypes.c_int32), ("bias_str", ctypes.c_int64 * 4),
+        ("has_mask", ctypes.c_int32), ("mask_str", ctypes.c_int64 * 2),
+        ("has_gate", ctypes.c_int32),
+    ]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libevoattn.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                raise RuntimeError(
+                    f"{_LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g;"
+                    " g.build()'` (no CPU or PyTorch fallback exists)")
+            lib = ctypes.CDLL(_LIB_PATH)
+            vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+            dp = ctypes.POINTER(Desc)
+            lib.evo_attn_validate.argtypes = [dp]
+            lib.evo_attn_validate.restype = i32
+            lib.evo_attn_fwd.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+            lib.evo_attn_fwd.restype = i32
+            lib.evo_attn_bwd_workspace_bytes.argtypes = [dp]
+            lib.evo_attn_bwd_workspace_bytes.restype = sz
+            lib.evo_attn_bwd.argtypes = [dp] + [vp] * 15 + [sz, vp]
+            lib.evo_attn_bwd.restype = i32
+            lib.evo_status_string.argtypes = [i32]
+            lib.evo_status_string.restype = ctypes.c_char_p
+            lib.evo_last_error_detail.restype = ctypes.c_char_p
+            lib.evo_abi_version.restype = i32
+            lib.evo_last_launch_count.restype = i32
+            _lib = lib
+    return _lib
+
+
+def last_launch_count() -> int:
+    return int(load().evo_last_launch_count())
+
+
+def _check(rc):
+    if rc != 0:
+        raise EvoError(rc, load().evo_last_error_detail().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _str3(t):
+    s = t.stride()
+    if t.size(-1) > 1 and s[-1] != 1:
+        raise ValueError("head dimension must be unit-stride")
+    return (ctypes.c_int64 * 3)(s[0], s[1], s[2])
+
+
+def make_desc(q, k, v, bias=None, mask=None, g=None, o=None, scale=None) -> Desc:
+    """Build the descriptor for logical views q,k,v(,g,o) [B,H,L,D], bias [H|B,H,Lq,Lk]."""
+    B, H, Lq, D = q.shape
+    Lk = k.shape[2]
+    if k.shape != (B, H, Lk, D) or v.shape != (B, H, Lk, D):
+        raise ValueError(f"q {tuple(q.shape)} / k {tuple(k.shape)} / v {tuple(v.shape)} mismatch")
+    d = Desc()
+    d.B, d.H, d.Lq, d.Lk, d.D = B, H, Lq, Lk, D
+    if q.dtype == torch.bfloat16:
+        d.dtype = EVO_BF16
+    elif q.dtype == torch.float32:
+        d.dtype = EVO_F32
+    else:
+        raise TypeError(f"dtype {q.dtype} not supported (bf16, or fp32 verification mode)")
+    for t in (k, v, g, bias, o):
+        if t is not None and t.dtype != q.dtype:
+            raise TypeError("q, k, v, g, bias, o must share one dtype")
+    d.scale = float(scale) if scale is not None else float(torch.tensor(D ** -0.5,
+                                                                       dtype=torch.float32))
+    d.q_str, d.k_str, d.v_str = _str3(q), _str3(k), _str3(v)
+    if o is not None:
+        d.o_str = _str3(o)
+    if g is not None:
+        if g.shape != q.shape:
+            raise ValueError("g must have q's shape")
+        d.g_str, d.has_gate = _str3(g), 1
+    if bias is not None:
+        if bias.dim() == 3 and tuple(bias.shape) == (H, Lq, Lk):
+            d.bias_kind = EVO_BIAS_SHARED
+            s = bias.stride()
+            d.bias_str = (ctypes.c_int64 * 4)(0, s[0], s[1], s[2])
+        elif bias.dim() == 4 and tuple(bias.shape) == (B, H, Lq, Lk):
+            d.bias_kind = EVO_BIAS_PER_BATCH
+            d.bias_str = (ctypes.c_int64 * 4)(*bias.stride())
+        else:  # bias shape neither [B,H,L,L] nor [H,L,L] -> shape error
+            raise ValueError(f"bias shape {tuple(bias.shape)} is neither [H,Lq,Lk] nor [B,H,Lq,Lk]")
+    if mask is not None:
+        if tuple(mask.shape) != (B, Lk) or mask.dtype not in (torch.uint8, torch.bool):
+            raise ValueError("mask must be uint8/bool [B, Lk]")
+        d.has_mask = 1
+        d.mask_str = (ctypes.c_int64 * 2)(*mask.stride())
+    return d
+
+
+def _alloc_like(t, dtype=None):
+    """Output buffer with exactly t's strides (the ABI writes dq/dk/dv/dg/dbias with the
+    strides of q/k/v/g/bias)."""
+    dtype = t.dtype if dtype is None else dtype
+    return torch.empty_strided(tuple(t.shape), tuple(t.stride()), dtype=dtype, device=t.device)
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def fwd(q, k, v, bias=None, mask=None, g=None, scale=None, out=None, stream=None):
+    """Forward.  Returns (o, lse); o has q's memory layout (``empty_like``)."""
+    o = torch.empty_like(q) if out is None else out  # preserve_format: q's layout when dense
+    B, H, Lq, _ = q.shape
+    lse = torch.empty((B, H, Lq), dtype=torch.float32, device=q.device)
+    d = make_desc(q, k, v, bias, mask, g, o, scale)
+    m = mask.view(torch.uint8) if (mask is not None and mask.dtype == torch.bool) else mask
+    _check(load().evo_attn_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(bias), _ptr(m),
+                               _ptr(g), _ptr(o), _ptr(lse), _stream(stream)))
+    return o, lse
+
+
+def workspace_bytes(q, k, v, bias=None, mask=None, g=None, scale=None) -> int:
+    d = make_desc(q, k, v, bias, mask, g, q, scale)
+    return int(load().evo_attn_bwd_workspace_bytes(ctypes.byref(d)))
+
+
+def bwd(q, k, v, o, lse, dout, bias=None, mask=None, g=None, scale=None, workspace=None,
+        stream=None, dbias_out=None):
+    """Backward.  Returns dict dq, dk, dv, dg (None without gate), dbias (fp32, bias layout;
+    None without bias)."""
+    if dout.stride() != o.stride():
+        dout = dout.contiguous() if o.is_contiguous() else torch.empty_like(o).copy_(dout)
+    d = make_desc(q, k, v, bias, mask, g, o, scale)
+    ws_need = int(load().evo_attn_bwd_workspace_bytes(ctypes.byref(d)))
+    if workspace is None or workspace.numel() < ws_need:
+        workspace = torch.empty(max(ws_need, 1), dtype=torch.uint8, device=q.device)
+    dq, dk, dv = _alloc_like(q), _alloc_like(k), _alloc_like(v)
+    dg = _alloc_like(g) if g is not None else None
+    dbias = None
+    if bias is not None:
+        dbias = _alloc_like(bias, torch.float32) if dbias_out is None else dbias_out
+        if dbias.stride() != bias.stride():
+            raise ValueError("dbias must have bias's strides (the library writes it that way)")
+    m = mask.view(torch.uint8) if (mask is not None and mask.dtype == torch.bool) else mask
+    _check(load().evo_attn_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(bias), _ptr(m),
+                               _ptr(g), _ptr(o), _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk),
+                               _ptr(dv), _ptr(dg), _ptr(dbias), _ptr(workspace), ws_need,
+                               _stream(stream)))
+    return {"dq": dq, "dk": dk, "dv": dv, "dg": dg, "dbias": dbias}
+
+
+def pad_bias(bias):
+    """Return a view of ``bias`` whose non-unit strides are multiples of 16 bytes (TMA rule in
+    evo_attn.h); copies only when needed.  Layout marshalling, not arithmetic."""
+    if bias is None:
+        return None
+    es = bias.element_size()
+    last = bias.size(-1)
+    if bias.stride(-1) == 1 and all((s * es) % 16 == 0 for s, n in
+                                    zip(bias.stride()[:-1], bias.shape[:-1]) if n > 1):
+        return bias
+    mult = 16 // es
+    lp = (last + mult - 1) // mult * mult
+    buf = torch.zeros(*bias.shape[:-1], lp, dtype=bias.dtype, device=bias.device)
+    buf[..., :last].copy_(bias)
+    return buf[..., :last]
+
+
+class EvoAttentionFunction(torch.autograd.Function):
+    """o = sigmoid(g) ⊙ softmax(scale·q·kᵀ + bias, masked)·v through the C ABI."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, bias, g, mask, scale):
+        bias_p = pad_bias(bias)
+        o, lse = fwd(q, k, v, bias_p, mask, g, scale)
+        ctx.save_for_backward(q, k, v, bias_p, g, mask, o, lse)
+        ctx.scale = scale
+        ctx.bias_orig = bias is not None
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, bias_p, g, mask, o, lse = ctx.saved_tensors
+        r = bwd(q, k, v, o, lse, do, bias_p, mask, g, ctx.scale)
+        db = r["dbias"]
+        if db is not None:
+            db = db.to(bias_p.dtype)
+        return r["dq"], r["dk"], r["dv"], db, r["dg"], None, None
+
+
+def evo_attention(q, k, v, bias=None, g=None, mask=None, scale=None):
+    """Differentiable gated pair-bias attention (bf16 or fp32-verification inputs)."""
+    return EvoAttentionFunction.apply(q, k, v, bias, g, mask, scale)

@@ -1,0 +1,105 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  bf16 I/O: every output within normwise max relative error 2e-2; fp32 verification mode:
+1e-5 (north star; reading R9).  Shapes span several 128-tiles and ragged tails."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_harness import rel_err, run_case
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-5}
+
+
+def _assert(errs, dtype, ctx=""):
+    bad = {k: v for k, v in errs.items() if not v <= TOL[dtype]}
+    assert not bad, f"{ctx} errors over {TOL[dtype]}: {bad} (all: {errs})"
+
+
+# (B, H, L, D, bias, bias_t, gate, mask, mask_t, layout)
+CASES = [
+    (2, 2, 128, 32, "shared", False, True, "prefix", False, "blhd"),     # one tile
+    (3, 2, 256, 32, "shared", False, True, "prefix_fm", False, "blhd"),  # 2x2 tiles, padded rows
+    (2, 3, 100, 32, "shared", False, True, "prefix", False, "bhld"),     # ragged single tile
+    (2, 2, 200, 16, "shared", False, False, "none", False, "blhd"),      # ragged 2 tiles, D=16
+    (2, 2, 129, 8, None, False, True, "prefix", True, "lbhd"),           # col-attn view, D=8
+    (2, 2, 300, 64, "shared", False, True, "prefix", False, "blhd"),     # D=64, 3 tiles
+    (2, 2, 256, 32, "shared", True, True, "prefix", True, "lbhd"),       # end-node view
+    (2, 2, 130, 32, "batch", False, True, "prefix", False, "blhd"),      # per-batch bias
+    (1, 1, 1, 16, "shared", False, True, "none", False, "bhld"),         # L = 1
+    (2, 2, 17, 32, "shared", True, False, "prefix", False, "blhd"),      # tiny ragged, bias^T
+    (2, 1, 384, 32, "shared", False, True, "prefix", False, "blhd"),     # cfg5-like L
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
+def test_bf16_parity(case):
+    B, H, L, D, bias, bias_t, gate, mask, mask_t, layout = case
+    errs, _, _ = run_case(B, H, L, L, D, seed=1, bias=bias, bias_t=bias_t, gate=gate, mask=mask,
+                          mask_t=mask_t, layout=layout)
+    _assert(errs, torch.bfloat16, str(case))
+
+
+@pytest.mark.parametrize("case", CASES[:8], ids=[str(c) for c in CASES[:8]])
+def test_f32_verification_parity(case):
+    B, H, L, D, bias, bias_t, gate, mask, mask_t, layout = case
+    errs, _, _ = run_case(B, H, L, L, D, seed=2, bias=bias, bias_t=bias_t, gate=gate, mask=mask,
+                          mask_t=mask_t, layout=layout, dtype=torch.float32)
+    _assert(errs, torch.float32, str(case))
+
+
+def test_unequal_lengths():
+    errs, _, _ = run_case(2, 2, 70, 200, 32, seed=3, bias="shared", mask="prefix")
+    _assert(errs, torch.bfloat16)
+
+
+def test_seeds_cfg1_shape():
+    for seed in range(5):
+        errs, _, _ = run_case(32, 2, 32, 32, 16, seed=seed, bias="shared", mask="prefix_fm")
+        _assert(errs, torch.bfloat16, f"seed {seed}")
+
+
+def test_fully_masked_rows_are_zero():
+    errs, out, c = run_case(4, 2, 64, 64, 32, seed=4, mask="prefix", bwd=True)
+    m = c["mask"].copy()
+    errs, out, c = run_case(4, 2, 64, 64, 32, seed=4, bwd=True, case=dict(
+        c, mask=np.where(np.arange(4)[:, None] == 2, 0, m).astype(np.uint8)))
+    assert torch.all(out["o"][2] == 0)
+    assert torch.all(torch.isneginf(out["lse"][2]))
+    assert torch.all(out["dq"][2] == 0) and torch.all(out["dg"][2] == 0)
+    assert torch.all(out["dk"][2] == 0) and torch.all(out["dv"][2] == 0)
+    _assert(errs, torch.bfloat16)
+
+
+def test_masked_keys_inert_bitwise():
+    """P4 on the GPU: re-randomising K/V/bias at masked keys changes no output bit."""
+    _, out1, c = run_case(2, 2, 192, 192, 32, seed=5, mask="prefix")
+    rng = np.random.default_rng(0)
+    c2 = dict(c)
+    k, v, b = c["k"].copy(), c["v"].copy(), c["bias"].copy()
+    drop = c["mask"] == 0
+    for bb in range(2):
+        idx = np.nonzero(drop[bb])[0]
+        k[bb, :, idx] = np.round(rng.standard_normal(k[bb, :, idx].shape) * 8)
+        v[bb, :, idx] = np.round(rng.standard_normal(v[bb, :, idx].shape) * 8)
+    c2.update(k=k, v=v, bias=b)
+    _, out2, _ = run_case(2, 2, 192, 192, 32, case=c2)
+    for n in ("o", "lse", "dq", "dg", "dbias"):
+        assert torch.equal(out1[n], out2[n]), n
+
+
+def test_deterministic():
+    _, a, _ = run_case(4, 2, 256, 256, 32, seed=6, mask="prefix")
+    _, b, _ = run_case(4, 2, 256, 256, 32, seed=6, mask="prefix")
+    for n in ("o", "lse", "dk", "dv", "dg", "dbias"):
+        assert torch.equal(a[n], b[n]), n
+
+
+def test_gradient_identities():
+    """P7 on the GPU output: Σ_k dbias = 0 and Σ_k dK = 0 (to bf16 accuracy)."""
+    _, out, c = run_case(8, 2, 256, 256, 32, seed=7, mask="none")
+    db = out["dbias"].double()
+    assert float(db.sum(-1).abs().max()) <= 2e-2 * float(db.abs().max()) * 16
+    dk = out["dk"].double()
+    assert float(dk.sum(2).abs().max()) <= 2e-2 * float(dk.abs().max()) * 16
