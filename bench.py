@@ -1,0 +1,484 @@
+#!/usr/bin/env python
+"""Benchmark: Evoformer gated pair-bias attention, fwd+bwd, one Evoformer block at N_res=256.
+
+BASELINE.json metric: "Evoformer attn fwd+bwd TFLOP/s & ms/block at N_res=256 (1/2/4/8 B200,
+% peak)".  One step = the four attention modules of one Evoformer block (row,
+column, triangle start, triangle end), each forward + backward through the C ABI, on seeded
+synthetic tensors shaped like OpenFold/MLPerf initial training (N_res=256, N_seq=128,
+8/4 heads of 32; BASELINE.json configs 2-3 + the block's MSA column attention):
+
+  row    B=N_seq=128  H=8 L=N_res=256 D=32  shared bias b_ij   (msa_mask rows)
+  col    B=N_res=256  H=8 L=N_seq=128 D=32  no bias            (msa_mask columns, strided view)
+  start  B=N_res=256  H=4 L=N_res=256 D=32  shared bias b_jk   (pair_mask rows)
+  end    B=N_res=256  H=4 L=N_res=256 D=32  bias b_ki (q-contiguous view), strided q/k/v/mask
+
+value = algorithmic TFLOP/s = Σ 12·B·H·L²·D over the four calls ÷ device time per step
+(the bwd recompute of S is not credited).  Projections / LayerNorm are outside the
+attention core and excluded.  Under torchrun (N > 1) the block runs under Dynamic Axial
+Parallelism (paper_2404_11068_b200/dap.py): rank r holds N_seq/N MSA rows and N_res/N pair rows,
+NCCL all-to-all transposes between row and column phases, bias all-gather / dbias
+reduce-scatter; value = whole-job TFLOP/s with max-over-ranks device time ("scaling": "strong").
+
+`--impl reference` times the fp64 CPU oracle (the only reference that exists: the paper ships no
+code) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Evoformer attn fwd+bwd TFLOP/s & ms/block at N_res=256 (1/2/4/8 B200, % peak)"
+N_RES, N_SEQ, C_HEAD = 256, 128, 32
+MODULES = [  # name, B, H, L, bias
+    ("row", N_SEQ, 8, N_RES, True),
+    ("col", N_RES, 8, N_SEQ, False),
+    ("start", N_RES, 4, N_RES, True),
+    ("end", N_RES, 4, N_RES, True),
+]
+
+
+def alg_flops(B, H, L, D):
+    return 12.0 * B * H * L * L * D
+
+
+def kernel_alg(name, B, H, L, D, bias):
+    """Algorithmic work of one launch of kernel `name` on a (B,H,L,L,D) call:
+    returns (flops, bytes, exps)."""
+    X = B * H * L * D  # elements of one [B,H,L,D] tensor
+    P = B * H * L * L  # score elements
+    bb = 2 * H * L * L if bias else 0
+    if name == "fwd_bf16":  # q,k,v,g in, o out (bf16); bias; mask; lse out
+        return 4.0 * P * D, 10.0 * X + bb + B * L + 4 * B * H * L, float(P)
+    if name == "bwd_pre":  # o, dO, g in; dA, dg out (bf16); lse in; D, lse2 out (fp32)
+        return 0.0, 10.0 * X + 12.0 * B * H * L, 0.0
+    if name == "bwd_main":  # q,k,v,dA in; dq,dk,dv out; lse2/D in; bias; mask
+        return 8.0 * P * D, 14.0 * X + 8.0 * B * H * L + bb + B * L, float(P)
+    if name == "bwd_bias":  # dbias (fp32) written once; inputs already counted in bwd_main
+        return 0.0, 2.0 * bb, float(P)
+    if name in ("dq_convert",):
+        return 0.0, 6.0 * X, 0.0
+    if name == "dbias_reduce":
+        return 0.0, 2.0 * bb, 0.0
+    return 0.0, 0.0, 0.0
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        busy = [s for s in sms if mx and s > 0.3 * mx] or sms
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ----------------------------------------------------------------------------- peaks
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- workload
+def make_module_inputs(torch, dev, name, B, H, L, bias, seed):
+    """Seeded synthetic inputs in the projection storage layouts of DESIGN.md §4."""
+    from synth.gen import round_bf16  # noqa: F401  (same recipe as the parity tests)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    D = C_HEAD
+    if name in ("row", "start"):  # storage [B, L, H, D] (m[s,r] / z[i,j] projections)
+        shape, perm = (B, L, H, D), (0, 2, 1, 3)
+    else:  # col / end: batch axis is the 2nd storage axis: storage [L, B, H, D]
+        shape, perm = (L, B, H, D), (1, 2, 0, 3)
+    t = {}
+    for n in ("q", "k", "v", "g", "dout"):
+        t[n] = torch.randn(shape, generator=g).to(dev, torch.bfloat16).permute(*perm)
+    t["bias"] = None
+    if bias:
+        bt = torch.randn((H, L, L), generator=g).to(dev, torch.bfloat16)
+        t["bias"] = bt.transpose(1, 2) if name == "end" else bt  # b_ki: q-contiguous view
+    m = torch.ones((B, L), dtype=torch.uint8)
+    t["mask"] = m.t().contiguous().to(dev).t() if name in ("col", "end") else m.to(dev)
+    return t
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_block_sample(batch_rows, seed=0):
+    """fp64 oracle fwd+bwd on `batch_rows` batch rows of each of the four modules (all heads).
+    Returns (algorithmic flops done, seconds)."""
+    import oracle
+    from synth.gen import attention_case
+    flops, secs = 0.0, 0.0
+    for i, (name, B, H, L, bias) in enumerate(MODULES):
+        b = min(batch_rows, B)
+        c = attention_case(b, H, L, L, C_HEAD, seed=seed + i, bias="shared" if bias else None,
+                           gate=True, mask="ones")
+        t0 = time.perf_counter()
+        oracle.attn_fwd(c["q"], c["k"], c["v"], c["bias"], c["mask"], c["g"], c["scale"])
+        oracle.attn_bwd(c["q"], c["k"], c["v"], c["dout"], c["bias"], c["mask"], c["g"],
+                        c["scale"])
+        secs += time.perf_counter() - t0
+        flops += alg_flops(b, H, L, C_HEAD)
+    return flops, secs
+
+
+def cpu_baseline(target_s=12.0):
+    import oracle
+    rows = 1
+    f, s = oracle_block_sample(rows)
+    while s < target_s / 4 and rows < 64:
+        rows *= 2
+        f, s = oracle_block_sample(rows)
+    return {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"fp64 C oracle (OpenMP), fwd+bwd of {rows} batch row(s) of each of the 4 "
+                      f"block modules (all heads, full L), {s:.1f} s; scaled by algorithmic flops",
+            "seconds": s}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    rows = args.ref_rows
+    times, flops = [], 0.0
+    for _ in range(args.warmup):
+        oracle_block_sample(rows)
+    for s in range(args.steps):
+        f, t = oracle_block_sample(rows, seed=s)
+        times.append(t)
+        flops = f
+    tot = sum(times)
+    value = flops * len(times) / tot / 1e12
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "evoformer_block_attn_nres256_nseq128_sample",
+                   "batch_rows_per_module": rows, "note": "bounded sample: the oracle runs "
+                   f"{rows} batch row(s) of each module per step (full block = 128/256 rows)"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": oracle.num_threads(),
+                         "kind": "oracle",
+                         "sample": f"{rows} batch row(s) per module per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    from paper_2404_11068_b200 import evoattn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2404_11068_b200 import dap_bench
+        return dap_bench.run(args, METRIC)
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    from paper_2404_11068_b200 import build as _b
+    _b.build_attn()  # no-op unless a source is newer than the in-tree .so
+    lib = evoattn.load()
+    stream = torch.cuda.current_stream()
+    mods = []
+    for i, (name, B, H, L, bias) in enumerate(MODULES):
+        t = make_module_inputs(torch, dev, name, B, H, L, bias, seed=100 + i)
+        ws = torch.empty(max(1, evoattn.workspace_bytes(t["q"], t["k"], t["v"], t["bias"],
+                                                        t["mask"], t["g"])),
+                         dtype=torch.uint8, device=dev)
+        mods.append((name, B, H, L, bias, t, ws))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        launches = 0
+        for name, B, H, L, bias, t, ws in mods:
+            o, lse = evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
+            launches += evoattn.last_launch_count()
+            evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"], t["mask"], t["g"],
+                        workspace=ws)
+            launches += evoattn.last_launch_count()
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, L2 flushed (256 MB write) before each, CUDA events per step
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    nk_per_step = 64
+    trace_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nk_per_step * args.steps)]
+    for e in trace_ev:  # torch creates events lazily: materialise the handles first
+        e.record(stream)
+    torch.cuda.synchronize()
+    trace_arr = (__import__("ctypes").c_void_p * len(trace_ev))(*[e.cuda_event for e in trace_ev])
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    lib.evo_trace_enable(trace_arr, len(trace_ev))
+    launches = 0
+    for s in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        ev[s][0].record(stream)
+        launches += step()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    ntr = lib.evo_trace_count()
+    labels = [lib.evo_trace_label(i).decode() for i in range(ntr)]
+    lib.evo_trace_enable(None, 0)
+    clk = clocks.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    ms_step = float(np.mean(ms))
+    flops = sum(alg_flops(B, H, L, C_HEAD) for _, B, H, L, _ in MODULES)
+    value = flops / (ms_step * 1e-3) / 1e12
+
+    # per-kernel device time (trace events) and the dominant kernel's roofline
+    per = {}
+    for i, lab in enumerate(labels):
+        per.setdefault(lab, []).append(trace_ev[2 * i].elapsed_time(trace_ev[2 * i + 1]))
+    # algorithmic work per launch, per kernel kind, averaged over the four modules
+    calls = []
+    for name, B, H, L, bias in MODULES:
+        calls.append(("fwd_bf16", B, H, L, bias))
+        calls += [("bwd_pre", B, H, L, bias), ("bwd_main", B, H, L, bias)]
+        if L > 128:
+            calls.append(("dq_convert", B, H, L, bias))
+        if bias:
+            calls += [("bwd_bias", B, H, L, bias), ("dbias_reduce", B, H, L, bias)]
+    work = {}
+    for kname, B, H, L, bias in calls:
+        f, by, ex = kernel_alg(kname, B, H, L, C_HEAD, bias)
+        w = work.setdefault(kname, [0.0, 0.0, 0.0, 0])
+        w[0] += f; w[1] += by; w[2] += ex; w[3] += 1
+    tot_traced = sum(sum(v) for v in per.values())
+    kernels = {}
+    for k, v in per.items():
+        n = len(v)
+        w = work.get(k, [0, 0, 0, 1])
+        per_launch_ms = sum(v) / n
+        f, by, ex = w[0] / w[3], w[1] / w[3], w[2] / w[3]
+        kernels[k] = {"launches": n, "ms_per_launch": per_launch_ms,
+                      "share": sum(v) / tot_traced,
+                      "tflops": f / (per_launch_ms * 1e-3) / 1e12,
+                      "gbs": by / (per_launch_ms * 1e-3) / 1e9,
+                      "gexps": ex / (per_launch_ms * 1e-3) / 1e9}
+    dom = max(kernels, key=lambda k: kernels[k]["share"])
+    pk = measured_peaks()
+    sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+    mufu_peak = 148 * 16 * sm_mhz * 1e6 / 1e9  # Gex2/s (16 ex2/clk/SM)
+    dk = kernels[dom]
+    fr_t = dk["tflops"] / pk["bf16_tflops"]
+    fr_h = dk["gbs"] / pk["hbm_gbs"]
+    fr_x = dk["gexps"] / mufu_peak
+    if fr_x >= max(fr_t, fr_h):
+        roof = {"bound": "alu", "achieved": dk["gexps"], "peak": mufu_peak, "unit": "Gexp2/s",
+                "frac": fr_x}
+    elif fr_h >= fr_t:
+        roof = {"bound": "hbm", "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": fr_h}
+    else:
+        roof = {"bound": "tensor", "achieved": dk["tflops"], "peak": pk["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": fr_t}
+    roof.update({"kernel": dom, "traffic": load_traffic(dom), "peak_source": pk["source"],
+                 "fracs": {"tensor": fr_t, "hbm": fr_h, "mufu": fr_x},
+                 "mufu_peak_note": f"148 SM x 16 ex2/clk x {sm_mhz:.0f} MHz (median SM clock "
+                                   "under load)"})
+
+    # e2e: host buffers through the same C ABI, h2d + d2h inside the timed region
+    e2e = run_e2e(torch, evoattn, mods, args, dev, stream, flops)
+
+    cpu = cpu_baseline(args.cpu_seconds) if not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "ms_per_block": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "evoformer_block_attn_nres256_nseq128",
+                   "modules": {m[0]: {"B": m[1], "H": m[2], "L": m[3], "D": C_HEAD,
+                                      "bias": m[4]} for m in MODULES},
+                   "l2": "flushed (256 MB write) before every timed step" if not args.no_flush
+                   else "warm", "parallelism": "single GPU"},
+        "pct_of_peak": {"tensor_measured": value / pk["bf16_tflops"],
+                        "tensor_nominal": value / 2250.0},
+        "roofline": roof,
+        "kernels": kernels,
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu capture summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get(kernel)
+        except Exception:
+            return None
+    return None
+
+
+def run_e2e(torch, evoattn, mods, args, dev, stream, flops):
+    """Same metric through the public API from pinned HOST buffers: every step copies its
+    inputs H2D and all results (o, lse, dq, dk, dv, dg, dbias) D2H inside the timed region."""
+    host = []
+    h2d = d2h = 0
+    for name, B, H, L, bias, t, ws in mods:
+        hin = {}
+        for n in ("q", "k", "v", "g", "dout", "bias", "mask"):
+            x = t[n]
+            if x is None:
+                continue
+            base = x if x.is_contiguous() else x  # keep the storage layout of the device view
+            hb = torch.empty_strided(base.shape, base.stride(), dtype=base.dtype,
+                                     pin_memory=True)
+            hb.copy_(base)
+            hin[n] = hb
+            h2d += x.numel() * x.element_size()
+        outs = {"o": torch.empty_like(t["q"]), "lse": torch.empty((B, H, L), device=dev)}
+        hout = {"o": torch.empty_strided(t["q"].shape, t["q"].stride(), dtype=torch.bfloat16,
+                                         pin_memory=True),
+                "lse": torch.empty((B, H, L), pin_memory=True),
+                "dq": torch.empty_strided(t["q"].shape, t["q"].stride(), dtype=torch.bfloat16,
+                                          pin_memory=True),
+                "dk": torch.empty_strided(t["k"].shape, t["k"].stride(), dtype=torch.bfloat16,
+                                          pin_memory=True),
+                "dv": torch.empty_strided(t["v"].shape, t["v"].stride(), dtype=torch.bfloat16,
+                                          pin_memory=True),
+                "dg": torch.empty_strided(t["g"].shape, t["g"].stride(), dtype=torch.bfloat16,
+                                          pin_memory=True)}
+        if bias:
+            hout["dbias"] = torch.empty_strided(t["bias"].shape, t["bias"].stride(),
+                                                dtype=torch.float32, pin_memory=True)
+        for n, hb in hout.items():
+            d2h += hb.numel() * hb.element_size()
+        host.append((t, ws, hin, hout))
+
+    def step():
+        for t, ws, hin, hout in host:
+            for n, hb in hin.items():
+                t[n].copy_(hb, non_blocking=True)
+            o, lse = evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
+            r = evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"], t["mask"],
+                            t["g"], workspace=ws)
+            hout["o"].copy_(o, non_blocking=True)
+            hout["lse"].copy_(lse, non_blocking=True)
+            for n in ("dq", "dk", "dv", "dg", "dbias"):
+                if n in hout:
+                    hout[n].copy_(r[n], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, 10))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / n
+    return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n,
+            "note": "pinned host buffers; all inputs H2D and all outputs D2H every step"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["evo", "reference"], default="evo")
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-rows", type=int, default=2,
+                    help="--impl reference: batch rows of each module per step")
+    ap.add_argument("--nseq", type=int, default=None, help="(DAP) override N_seq")
+    ap.add_argument("--nres", type=int, default=None, help="(DAP) override N_res")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -117,6 +117,15 @@ int evo_abi_version(void);
    (memsets excluded); used by bench.py to report gpu_launches. */
 int evo_last_launch_count(void);
 
+/* Profiling hook (bench.py): while enabled on the calling thread, every kernel that
+   evo_attn_fwd / evo_attn_bwd launches is bracketed by cudaEventRecord on the call's stream into
+   caller-created events: kernel i runs between events[2i] and events[2i+1]; its name is
+   evo_trace_label(i).  `events` is an array of cudaEvent_t; NULL disables.  Returns 0, or
+   EVO_E_INVALID for a negative capacity.  Recording stops silently when capacity is reached. */
+int evo_trace_enable(void** events, int capacity);
+int evo_trace_count(void);           /* kernels recorded since evo_trace_enable */
+const char* evo_trace_label(int i);  /* NULL if out of range */
+
 #ifdef __cplusplus
 }
 #endif

@@ -164,11 +164,58 @@ evo_status_t cuda_fail(cudaError_t e, const char* what) {
   return fail(EVO_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------------------ optional kernel tracing
+struct Trace {
+  cudaEvent_t* ev = nullptr;
+  int cap = 0, n = 0;
+  const char* labels[4096];
+};
+thread_local Trace g_trace;
+inline void trace_begin(cudaStream_t st, const char* label) {
+  Trace& t = g_trace;
+  if (!t.ev || 2 * t.n + 1 >= t.cap || t.n >= 4096) return;
+  t.labels[t.n] = label;
+  if (cudaEventRecord(t.ev[2 * t.n], st) != cudaSuccess) {
+    (void)cudaGetLastError();  // a bad trace event must not poison the kernel launch
+    t.ev = nullptr;
+  }
+}
+inline void trace_end(cudaStream_t st) {
+  Trace& t = g_trace;
+  if (!t.ev || 2 * t.n + 1 >= t.cap || t.n >= 4096) return;
+  if (cudaEventRecord(t.ev[2 * t.n + 1], st) != cudaSuccess) {
+    (void)cudaGetLastError();
+    t.ev = nullptr;
+    return;
+  }
+  ++t.n;
+}
+// launch wrapper: bracket one kernel launch with trace events
+template <class F>
+inline cudaError_t traced(cudaStream_t st, const char* label, F&& f) {
+  trace_begin(st, label);
+  cudaError_t e = f();
+  trace_end(st);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
 
 int evo_abi_version(void) { return EVO_ATTN_ABI_VERSION; }
+
+int evo_trace_enable(void** events, int capacity) {
+  if (capacity < 0) return EVO_E_INVALID;
+  g_trace.ev = reinterpret_cast<cudaEvent_t*>(events);
+  g_trace.cap = events ? capacity : 0;
+  g_trace.n = 0;
+  return EVO_OK;
+}
+int evo_trace_count(void) { return g_trace.n; }
+const char* evo_trace_label(int i) {
+  return (i >= 0 && i < g_trace.n) ? g_trace.labels[i] : nullptr;
+}
 int evo_last_launch_count(void) { return g_launches; }
 const char* evo_last_error_detail(void) { return g_detail.c_str(); }
 
@@ -265,7 +312,7 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
     a.mask = mask; a.mask_s0 = d->mask_str[0]; a.mask_s1 = d->mask_str[1];
     a.o = (float*)o; a.o_sb = d->o_str[0]; a.o_sh = d->o_str[1]; a.o_sl = d->o_str[2];
     a.lse = lse;
-    cudaError_t e = evo::launch_fwd_f32(a, st);
+    cudaError_t e = traced(st, "fwd_f32", [&] { return evo::launch_fwd_f32(a, st); });
     g_launches = 1;
     return e == cudaSuccess ? EVO_OK : cuda_fail(e, "fwd_f32");
   }
@@ -287,7 +334,7 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
   a.g = (const __nv_bfloat16*)g; a.g_sb = d->g_str[0]; a.g_sh = d->g_str[1]; a.g_sl = d->g_str[2];
   a.o = (__nv_bfloat16*)o; a.o_sb = d->o_str[0]; a.o_sh = d->o_str[1]; a.o_sl = d->o_str[2];
   a.lse = lse;
-  cudaError_t e = evo::launch_fwd_bf16(L, dpad(d->D), bm, st);
+  cudaError_t e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_bf16(L, dpad(d->D), bm, st); });
   g_launches = 1;
   return e == cudaSuccess ? EVO_OK : cuda_fail(e, "fwd_bf16");
 }
@@ -331,7 +378,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   pa.o = o; pa.dout = dout; pa.o_sb = d->o_str[0]; pa.o_sh = d->o_str[1]; pa.o_sl = d->o_str[2];
   pa.g = g; pa.g_sb = d->g_str[0]; pa.g_sh = d->g_str[1]; pa.g_sl = d->g_str[2]; pa.dg = dg;
   pa.lse = lse; pa.lse2 = lse2; pa.Dvec = dvec; pa.dA = dA;
-  if ((e = evo::launch_bwd_pre(pa, d->dtype == EVO_F32, st)) != cudaSuccess) return cuda_fail(e, "bwd_pre");
+  if ((e = traced(st, "bwd_pre", [&] { return evo::launch_bwd_pre(pa, d->dtype == EVO_F32, st); })) != cudaSuccess) return cuda_fail(e, "bwd_pre");
   ++nl;
   // dA operand: workspace [B,H,Lq,D] contiguous, or dout itself when there is no gate
   const int64_t da_str[3] = {(int64_t)d->H * d->Lq * d->D, (int64_t)d->Lq * d->D, d->D};
@@ -352,7 +399,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     a.dA = (const float*)dA_ptr; a.a_sb = dA_str[0]; a.a_sh = dA_str[1]; a.a_sl = dA_str[2];
     a.lse_in = lse; a.Dvec = dvec;
     a.dq = (float*)dq; a.dk = (float*)dk; a.dv = (float*)dv; a.dbias = dbias;
-    e = evo::launch_bwd_f32(a, st, &nl);
+    e = traced(st, "bwd_f32", [&] { return evo::launch_bwd_f32(a, st, &nl); });
     g_launches = nl;
     return e == cudaSuccess ? EVO_OK : cuda_fail(e, "bwd_f32");
   }
@@ -386,13 +433,13 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   ma.dv = (__nv_bfloat16*)dv; ma.v_sb = d->v_str[0]; ma.v_sh = d->v_str[1]; ma.v_sl = d->v_str[2];
   ma.dq = (__nv_bfloat16*)dq; ma.q_sb = d->q_str[0]; ma.q_sh = d->q_str[1]; ma.q_sl = d->q_str[2];
   ma.dq_acc = dqacc;
-  if ((e = evo::launch_bwd_main_bf16(M, dpad(d->D), bm, st)) != cudaSuccess) return cuda_fail(e, "bwd_main");
+  if ((e = traced(st, "bwd_main", [&] { return evo::launch_bwd_main_bf16(M, dpad(d->D), bm, st); })) != cudaSuccess) return cuda_fail(e, "bwd_main");
   ++nl;
   if (dqacc) {
     evo::ConvertArgs ca{};
     ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
     ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
-    if ((e = evo::launch_dq_convert(ca, st)) != cudaSuccess) return cuda_fail(e, "dq_convert");
+    if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
     ++nl;
   }
   if (bm) {
@@ -407,7 +454,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     ba.mask = mask; ba.mask_s0 = d->mask_str[0]; ba.mask_s1 = d->mask_str[1];
     ba.lse2 = lse2; ba.Dvec = dvec;
     ba.partial = reinterpret_cast<float*>(ws + W.partial);
-    if ((e = evo::launch_bwd_bias_bf16(Bl, dpad(d->D), bm, st)) != cudaSuccess) return cuda_fail(e, "bwd_bias");
+    if ((e = traced(st, "bwd_bias", [&] { return evo::launch_bwd_bias_bf16(Bl, dpad(d->D), bm, st); })) != cudaSuccess) return cuda_fail(e, "bwd_bias");
     ++nl;
     evo::ReduceArgs ra{};
     const bool pb = d->bias_kind == EVO_BIAS_PER_BATCH;
@@ -416,7 +463,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     ra.partial = ba.partial; ra.dbias = dbias;
     ra.s_b = pb ? d->bias_str[0] : 0; ra.s_h = d->bias_str[1]; ra.s_q = d->bias_str[2]; ra.s_k = d->bias_str[3];
     ra.q_fast = bm == 2;
-    if ((e = evo::launch_dbias_reduce(ra, st)) != cudaSuccess) return cuda_fail(e, "dbias_reduce");
+    if ((e = traced(st, "dbias_reduce", [&] { return evo::launch_dbias_reduce(ra, st); })) != cudaSuccess) return cuda_fail(e, "dbias_reduce");
     ++nl;
   }
   g_launches = nl;

@@ -79,6 +79,11 @@ def load():
             lib.evo_last_error_detail.restype = ctypes.c_char_p
             lib.evo_abi_version.restype = i32
             lib.evo_last_launch_count.restype = i32
+            lib.evo_trace_enable.argtypes = [vp, i32]
+            lib.evo_trace_enable.restype = i32
+            lib.evo_trace_count.restype = i32
+            lib.evo_trace_label.argtypes = [i32]
+            lib.evo_trace_label.restype = ctypes.c_char_p
             _lib = lib
     return _lib
 
