@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -69,7 +70,7 @@ int bias_mode(const evo_attn_desc_t* d) {  // 0 none, 1 k-contiguous, 2 q-contig
 
 // Tensor map over a logical [B][H][L][D] tensor with element strides (b, h, l), unit d.
 bool make_x_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int es, int64_t B,
-                int64_t H, int64_t L, int D, const int64_t str[3]) {
+                int64_t H, int64_t L, int D, const int64_t str[3], int box_rows = 128) {
   auto enc = get_encode();
   if (!enc) return false;
   const int DP = dpad(D);
@@ -85,7 +86,7 @@ bool make_x_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int es,
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)std::max<int64_t>(L, 1),
                         (cuuint64_t)std::max<int64_t>(H, 1), (cuuint64_t)std::max<int64_t>(B, 1)};
   cuuint64_t strides[3] = {sb[2], sb[1], sb[0]};
-  cuuint32_t box[4] = {(cuuint32_t)DP, 128, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)DP, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   const int rowb = DP * es;
   CUtensorMapSwizzle sw = rowb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
@@ -97,7 +98,8 @@ bool make_x_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int es,
 }
 
 // Bias tile map: rows = non-contiguous index, cols = contiguous index; box 64 cols x 128 rows.
-bool make_bias_map(CUtensorMap* m, const evo_attn_desc_t* d, const void* bias) {
+bool make_bias_map(CUtensorMap* m, const evo_attn_desc_t* d, const void* bias,
+                   int box_rows = 128) {
   auto enc = get_encode();
   if (!enc) return false;
   const int mode = bias_mode(d);
@@ -118,7 +120,7 @@ bool make_bias_map(CUtensorMap* m, const evo_attn_desc_t* d, const void* bias) {
                         (cuuint64_t)std::max<int64_t>(r_ext, 1), (cuuint64_t)d->H,
                         (cuuint64_t)std::max<int64_t>(Bb, 1)};
   cuuint64_t strides[3] = {sb[2], sb[1], sb[0]};
-  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(bias), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -328,13 +330,37 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
     return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
   evo::FwdArgs& a = L.args;
   a.B = (int)d->B; a.H = d->H; a.Lq = d->Lq; a.Lk = d->Lk; a.D = d->D;
+  a.scale = d->scale;
   a.scale_log2 = d->scale * evo::kLog2e;
   a.bias_batched = d->bias_kind == EVO_BIAS_PER_BATCH;
   a.mask = mask; a.mask_s0 = d->mask_str[0]; a.mask_s1 = d->mask_str[1];
   a.g = (const __nv_bfloat16*)g; a.g_sb = d->g_str[0]; a.g_sh = d->g_str[1]; a.g_sl = d->g_str[2];
   a.o = (__nv_bfloat16*)o; a.o_sb = d->o_str[0]; a.o_sh = d->o_str[1]; a.o_sl = d->o_str[2];
   a.lse = lse;
-  cudaError_t e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_bf16(L, dpad(d->D), bm, st); });
+  static const bool dbg_timing = getenv("EVO_DEBUG_TIMING") != nullptr;
+  a.dbg = dbg_timing ? evo::fwd_debug_ptr() : nullptr;
+  static const int fwd_flags = getenv("EVO_FWD_FLAGS") ? atoi(getenv("EVO_FWD_FLAGS")) : 0;
+  a.flags = fwd_flags;
+  // kernel variant (A/B experiments only): "occ" (default), "ws", "v1"
+  static const char* impl = getenv("EVO_FWD_IMPL") ? getenv("EVO_FWD_IMPL") : "occ";
+  cudaError_t e;
+  if (!strcmp(impl, "occ")) {
+    evo::FwdOccLaunch O;
+    memset(&O, 0, sizeof(O));
+    if (!make_x_map(&O.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||
+        !make_x_map(&O.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 64) ||
+        (bm && !make_bias_map(&O.tm_b, d, bias, bm == 1 ? 128 : 64)))
+      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed (occ)");
+    O.args = a;
+    O.q = (const __nv_bfloat16*)q;
+    O.q_sb = d->q_str[0]; O.q_sh = d->q_str[1]; O.q_sl = d->q_str[2];
+    e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_occ_bf16(O, dpad(d->D), bm, st); });
+  } else {
+    e = traced(st, "fwd_bf16", [&] {
+      return !strcmp(impl, "v1") ? evo::launch_fwd_bf16(L, dpad(d->D), bm, st)
+                                 : evo::launch_fwd_ws_bf16(L, dpad(d->D), bm, st);
+    });
+  }
   g_launches = 1;
   return e == cudaSuccess ? EVO_OK : cuda_fail(e, "fwd_bf16");
 }

@@ -10,6 +10,7 @@ constexpr int kMaxLk = kMaxMaskWords * 32;
 // ------------------------------------------------------------------ forward (bf16, tcgen05)
 struct FwdArgs {
   int B, H, Lq, Lk, D;
+  float scale;       // logits = scale * q·k + bias
   float scale_log2;  // scale * log2(e)
   int bias_batched;  // per-batch bias: TMA coordinate 3 = b
   const uint8_t* mask;
@@ -19,6 +20,8 @@ struct FwdArgs {
   __nv_bfloat16* o;
   int64_t o_sb, o_sh, o_sl;
   float* lse;
+  unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
+  int flags;                // experiment switches (EVO_FWD_FLAGS), 0 in production
 };
 struct FwdLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_b;
@@ -28,6 +31,17 @@ inline size_t fwd_smem_bytes(int DP) {
   return 5 * 128 * (size_t)DP * 2 + 65536 + kMaxMaskWords * 4 + 2 * 256 * 4 + 8 * 8 + 16;
 }
 cudaError_t launch_fwd_bf16(const FwdLaunch& L, int DP, int bias_mode, cudaStream_t st);
+// persistent warp-specialised forward (evo_fwd_ws.cu)
+cudaError_t launch_fwd_ws_bf16(const FwdLaunch& L, int DP, int bias_mode, cudaStream_t st);
+unsigned long long* fwd_debug_ptr();
+// occupancy-based forward (evo_fwd_occ.cu): K/V maps with 64-row boxes, Q read by threads
+struct FwdOccLaunch {
+  CUtensorMap tm_k, tm_v, tm_b;
+  FwdArgs args;
+  const __nv_bfloat16* q;
+  int64_t q_sb, q_sh, q_sl;
+};
+cudaError_t launch_fwd_occ_bf16(const FwdOccLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
 // ------------------------------------------------------------------ backward (bf16)
 struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
