@@ -301,6 +301,12 @@ EVO_DEV bool mbar_try_wait(uint32_t bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// Spin on test_wait (never suspends): for single-thread control paths where a wake-up delay
+// sits on the critical path.
+EVO_DEV void mbar_wait_spin(uint32_t bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
 
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
 EVO_DEV void umma_commit(uint32_t bar) {
