@@ -241,7 +241,7 @@ def run_gpu(args):
     from paper_2404_11068_b200 import evoattn
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.dap:
         from paper_2404_11068_b200 import dap_bench
         return dap_bench.run(args, METRIC)
 
@@ -470,6 +470,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=2,
                     help="--impl reference: batch rows of each module per step")
+    ap.add_argument("--dap", action="store_true", help="run the DAP path even at N=1")
     ap.add_argument("--nseq", type=int, default=None, help="(DAP) override N_seq")
     ap.add_argument("--nres", type=int, default=None, help="(DAP) override N_res")
     args = ap.parse_args()

@@ -1,0 +1,162 @@
+"""bench.py's multi-GPU leg: one Evoformer block's attention core under DAP-N (dap.py), one
+process per GPU (torchrun), NCCL over NVLink/NVSwitch.
+
+Each rank holds its DAP shards of the N_res=256 / N_seq=128 block and runs fwd + bwd of the four
+modules on them with the block's 8 transposes, 3 bias all-gathers and 3 dbias reduce-scatters.
+Timing: W warm-up steps, then K steps bracketed by a barrier and cuda synchronize, CUDA events
+on the compute stream, max over ranks; value = the whole block's algorithmic flops ÷ that time
+(total work fixed: "scaling": "strong")."""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+
+def run(args, metric):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import build as _b
+    from . import dap, evoattn
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        _b.build_all()
+    if world > 1:
+        dist.barrier()
+    evoattn.load()
+    n_seq = args.nseq or 128
+    n_res = args.nres or 256
+    comm = dap.NcclDap()
+    loc, _ = dap.make_block_inputs(torch, world, rank, n_seq, n_res, seed=0, device=dev)
+    attn = _Counting(evoattn)
+    blk = dap.DapEvoformerAttention(comm, attn, loc)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        blk.forward()
+        return blk.backward(loc["dm_next"], loc["dz_next"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    from bench import ClockSampler  # noqa: E402  (repo root is on sys.path under bench.py)
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    comm.barrier()
+    torch.cuda.synchronize()
+    attn.launches = 0
+    for s in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        comm.barrier()  # stragglers show up as their own time
+        ev[s][0].record(stream)
+        step()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    clk = clocks.stop() if rank == 0 else None
+    flops = dap.block_flops(n_seq, n_res)
+    # our kernels in the timed region: the attention core's launches (C ABI count) + one
+    # pack/unpack per transpose when N > 1 (NCCL's own kernels are library code, not counted)
+    launches = attn.launches + (8 * args.steps if world > 1 else 0)
+    e2e = _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops)
+    if rank == 0:
+        line = {
+            "metric": metric, "value": flops / (ms_max * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "ms_per_block": ms_max, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"evoformer_block_attn_nres{n_res}_nseq{n_seq}",
+                       "parallelism": f"dap{world}", "local_shapes": dap.plan(world, n_seq, n_res),
+                       "l2": "flushed (256 MB write) before every timed step" if not args.no_flush
+                       else "warm",
+                       "collectives_per_block": {"a2a": 8, "allgather": 3, "reduce_scatter": 3}},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+class _Counting:
+    """evoattn with a running count of the kernels its calls launched (evo_last_launch_count)."""
+
+    def __init__(self, mod):
+        self.mod, self.launches = mod, 0
+
+    def fwd(self, *a, **k):
+        r = self.mod.fwd(*a, **k)
+        self.launches += self.mod.last_launch_count()
+        return r
+
+    def bwd(self, *a, **k):
+        r = self.mod.bwd(*a, **k)
+        self.launches += self.mod.last_launch_count()
+        return r
+
+
+def _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops):
+    """Same block through the same API from pinned HOST buffers: this rank's input shards are
+    copied H2D and its outputs (m_next, z_next and every gradient shard) D2H inside the timed
+    region; max over ranks."""
+    host_in = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v)
+               for k, v in loc.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host_in.values())
+    host_out = {}
+
+    def e2e_step():
+        for k, v in host_in.items():
+            loc[k].copy_(v, non_blocking=True)
+        m_next, z_next, _ = blk.forward()
+        grads = blk.backward(loc["dm_next"], loc["dz_next"])
+        outs = dict(grads, m_next=m_next, z_next=z_next)
+        for k, v in outs.items():
+            if v is None:
+                continue
+            if k not in host_out:
+                host_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+            host_out[k].copy_(v, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+    n = max(3, min(args.steps, 10))
+    blk.comm.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / n], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n,
+            "note": "per rank: pinned host shards H2D, outputs and gradient shards D2H"}
