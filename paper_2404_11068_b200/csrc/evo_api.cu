@@ -130,7 +130,16 @@ bool make_bias_map(CUtensorMap* m, const evo_attn_desc_t* d, const void* bias,
 struct WsLayout {
   size_t lse2 = 0, dvec = 0, da = 0, dqacc = 0, partial = 0, total = 0;
   int nchunks = 1, chunk = 1;
+  bool fused = false;
 };
+// Single-pass backward (evo_bwd_fused.cu) for bf16 with a shared bias or none and Lq <= 256;
+// EVO_BWD_IMPL=split forces the two-pass kernels (A/B experiments).
+bool use_fused_bwd(const evo_attn_desc_t* d) {
+  static const bool split = getenv("EVO_BWD_IMPL") && !strcmp(getenv("EVO_BWD_IMPL"), "split");
+  if (split || d->dtype != EVO_BF16 || d->bias_kind == EVO_BIAS_PER_BATCH) return false;
+  const int Lq_pad = ((d->Lq + 127) / 128) * 128;
+  return evo::bwd_fused_supported(dpad(d->D), Lq_pad, d->bias_kind != EVO_BIAS_NONE);
+}
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 WsLayout ws_layout(const evo_attn_desc_t* d) {
@@ -146,12 +155,20 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
     w.dqacc = off;
     off = al256(off + (size_t)rows * d->Lq * d->D * 4);
   }
+  w.fused = use_fused_bwd(d);
   if (d->dtype == EVO_BF16 && d->bias_kind != EVO_BIAS_NONE && d->B > 0) {
-    const int64_t tiles = (int64_t)d->H * nq * nk;
-    int64_t nch = (2 * kNumSMs + tiles - 1) / std::max<int64_t>(tiles, 1);
-    nch = std::max<int64_t>(1, std::min<int64_t>(nch, d->B));
-    const int64_t chunk = (d->B + nch - 1) / nch;
-    nch = (d->B + chunk - 1) / chunk;
+    int64_t nch, chunk;
+    if (w.fused) {
+      int ch = 1;
+      nch = evo::bwd_fused_nchunks((int)d->B, d->H, (int)nk, kNumSMs, &ch);
+      chunk = ch;
+    } else {
+      const int64_t tiles = (int64_t)d->H * nq * nk;
+      nch = (2 * kNumSMs + tiles - 1) / std::max<int64_t>(tiles, 1);
+      nch = std::max<int64_t>(1, std::min<int64_t>(nch, d->B));
+      chunk = (d->B + nch - 1) / nch;
+      nch = (d->B + chunk - 1) / chunk;
+    }
     w.nchunks = (int)nch;
     w.chunk = (int)chunk;
     const int64_t parts = d->bias_kind == EVO_BIAS_PER_BATCH ? d->B : nch;
@@ -445,6 +462,45 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (dqacc) {
     if ((e = cudaMemsetAsync(dqacc, 0, (size_t)d->B * d->H * d->Lq * d->D * 4, st)) != cudaSuccess)
       return cuda_fail(e, "memset dq_acc");
+  }
+  if (W.fused) {
+    evo::BwdFusedLaunch F;
+    F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
+    evo::BwdFusedArgs& fa = F.args;
+    memset(&fa, 0, sizeof(fa));
+    fa.B = (int)d->B; fa.H = d->H; fa.Lq = d->Lq; fa.Lk = d->Lk; fa.D = d->D;
+    fa.scale = d->scale; fa.scale_log2 = d->scale * evo::kLog2e;
+    // same chunking as the workspace's dbias partials (ws_layout)
+    fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, nk, kNumSMs, &fa.chunk);
+    fa.bias = (const __nv_bfloat16*)bias;
+    fa.b_sh = d->bias_str[1]; fa.b_sq = d->bias_str[2]; fa.b_sk = d->bias_str[3];
+    fa.mask = mask; fa.mask_s0 = d->mask_str[0]; fa.mask_s1 = d->mask_str[1];
+    fa.lse2 = lse2; fa.Dvec = dvec;
+    fa.dk = (__nv_bfloat16*)dk; fa.k_sb = d->k_str[0]; fa.k_sh = d->k_str[1]; fa.k_sl = d->k_str[2];
+    fa.dv = (__nv_bfloat16*)dv; fa.v_sb = d->v_str[0]; fa.v_sh = d->v_str[1]; fa.v_sl = d->v_str[2];
+    fa.dq = (__nv_bfloat16*)dq; fa.q_sb = d->q_str[0]; fa.q_sh = d->q_str[1]; fa.q_sl = d->q_str[2];
+    fa.dq_acc = dqacc;
+    fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
+    if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
+    ++nl;
+    if (dqacc) {
+      evo::ConvertArgs ca{};
+      ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
+      ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
+      if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
+      ++nl;
+    }
+    if (bm) {
+      evo::ReduceArgs ra{};
+      ra.nparts = fa.nchunks; ra.H = d->H; ra.Lq = d->Lq; ra.Lk = d->Lk; ra.nb = 1;
+      ra.partial = fa.partial; ra.dbias = dbias;
+      ra.s_b = 0; ra.s_h = d->bias_str[1]; ra.s_q = d->bias_str[2]; ra.s_k = d->bias_str[3];
+      ra.q_fast = bm == 2;
+      if ((e = traced(st, "dbias_reduce", [&] { return evo::launch_dbias_reduce(ra, st); })) != cudaSuccess) return cuda_fail(e, "dbias_reduce");
+      ++nl;
+    }
+    g_launches = nl;
+    return EVO_OK;
   }
   evo::BwdMainLaunch M;
   M.tm_q = tq; M.tm_k = tk; M.tm_v = tv; M.tm_da = tda; M.tm_b = tb;

@@ -106,6 +106,47 @@ inline size_t bwd_bias_smem_bytes(int DP) {
 }
 cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
+// Fused backward (evo_bwd_fused.cu): CTA per (h, 128-key tile, batch chunk); dK, dV, dQ parts
+// and the chunk's dbias partial in one pass (shared bias or none; Lq <= 256).
+struct BwdFusedArgs {
+  int B, H, Lq, Lk, D;
+  float scale, scale_log2;
+  int nchunks, chunk;
+  const __nv_bfloat16* bias;  // shared bias [h, q, k] with element strides below (or NULL)
+  int64_t b_sh, b_sq, b_sk;
+  const uint8_t* mask;
+  int64_t mask_s0, mask_s1;
+  const float* lse2;  // [B*H][Lq_pad]
+  const float* Dvec;
+  __nv_bfloat16* dk;
+  int64_t k_sb, k_sh, k_sl;
+  __nv_bfloat16* dv;
+  int64_t v_sb, v_sh, v_sl;
+  __nv_bfloat16* dq;  // direct store when there is a single key tile
+  int64_t q_sb, q_sh, q_sl;
+  float* dq_acc;      // [B,H,Lq,D] fp32 accumulator otherwise
+  float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
+};
+struct BwdFusedLaunch {
+  CUtensorMap tm_q, tm_k, tm_v, tm_da;
+  BwdFusedArgs args;
+};
+// eligibility + resources of the fused path for head-dim pad DP and padded Lq
+inline bool bwd_fused_supported(int DP, int Lq_pad, bool bias) {
+  const int cols = (bias ? Lq_pad : 0) + 128 + 3 * DP;
+  return Lq_pad <= 256 && cols <= 512 && DP >= 16;
+}
+inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
+  const int groups = H * nk;
+  int nch = num_sms / (groups > 0 ? groups : 1);
+  if (nch < 1) nch = 1;
+  if (nch > B) nch = B;
+  const int ch = (B + nch - 1) / nch;
+  *chunk = ch;
+  return (B + ch - 1) / ch;
+}
+cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st);
+
 struct ReduceArgs {  // dbias[h,q,k] (bias strides) = Σ_c partial[c][h][q][k]
   int nparts, H, Lq, Lk;
   int64_t nb;        // leading count of the destination (1 shared, B per-batch)
