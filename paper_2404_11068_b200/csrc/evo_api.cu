@@ -70,7 +70,8 @@ int bias_mode(const evo_attn_desc_t* d) {  // 0 none, 1 k-contiguous, 2 q-contig
 
 // Tensor map over a logical [B][H][L][D] tensor with element strides (b, h, l), unit d.
 bool make_x_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int es, int64_t B,
-                int64_t H, int64_t L, int D, const int64_t str[3], int box_rows = 128) {
+                int64_t H, int64_t L, int D, const int64_t str[3], int box_rows = 128,
+                int box_cols = 0) {
   auto enc = get_encode();
   if (!enc) return false;
   const int DP = dpad(D);
@@ -86,9 +87,10 @@ bool make_x_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int es,
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)std::max<int64_t>(L, 1),
                         (cuuint64_t)std::max<int64_t>(H, 1), (cuuint64_t)std::max<int64_t>(B, 1)};
   cuuint64_t strides[3] = {sb[2], sb[1], sb[0]};
-  cuuint32_t box[4] = {(cuuint32_t)DP, (cuuint32_t)box_rows, 1, 1};
+  const int bc = box_cols > 0 ? box_cols : DP;
+  cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  const int rowb = DP * es;
+  const int rowb = bc * es;
   CUtensorMapSwizzle sw = rowb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                      : (rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                    : CU_TENSOR_MAP_SWIZZLE_128B);
@@ -152,8 +154,9 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
   w.dvec = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   if (d->has_gate) { w.da = off; off = al256(off + (size_t)rows * d->Lq * d->D * esize(d)); }
   if (d->dtype == EVO_BF16 && nk > 1) {
-    w.dqacc = off;
-    off = al256(off + (size_t)rows * d->Lq * d->D * 4);
+    w.dqacc = off;  // fused: one fp32 dQ part per key tile (plain stores); split: one atomic sum
+    const int64_t parts = use_fused_bwd(d) ? nk : 1;
+    off = al256(off + (size_t)parts * rows * d->Lq * d->D * 4);
   }
   w.fused = use_fused_bwd(d);
   if (d->dtype == EVO_BF16 && d->bias_kind != EVO_BIAS_NONE && d->B > 0) {
@@ -421,6 +424,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   pa.o = o; pa.dout = dout; pa.o_sb = d->o_str[0]; pa.o_sh = d->o_str[1]; pa.o_sl = d->o_str[2];
   pa.g = g; pa.g_sb = d->g_str[0]; pa.g_sh = d->g_str[1]; pa.g_sl = d->g_str[2]; pa.dg = dg;
   pa.lse = lse; pa.lse2 = lse2; pa.Dvec = dvec; pa.dA = dA;
+  pa.negate = W.fused ? 1 : 0;
   if ((e = traced(st, "bwd_pre", [&] { return evo::launch_bwd_pre(pa, d->dtype == EVO_F32, st); })) != cudaSuccess) return cuda_fail(e, "bwd_pre");
   ++nl;
   // dA operand: workspace [B,H,Lq,D] contiguous, or dout itself when there is no gate
@@ -459,13 +463,23 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (bm && !make_bias_map(&tb, d, bias)) return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
 
   float* dqacc = nk > 1 ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
-  if (dqacc) {
+  if (dqacc && !W.fused) {
     if ((e = cudaMemsetAsync(dqacc, 0, (size_t)d->B * d->H * d->Lq * d->D * 4, st)) != cudaSuccess)
       return cuda_fail(e, "memset dq_acc");
   }
   if (W.fused) {
     evo::BwdFusedLaunch F;
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
+    // output maps for the TMA-store drains: dk/dv (bf16, k/v strides); dq (bf16, q strides)
+    // when there is one key tile, else the fp32 parts [nk*B][H][Lq][D] (32-column boxes)
+    const int64_t part_str[3] = {(int64_t)d->H * d->Lq * d->D, (int64_t)d->Lq * d->D, d->D};
+    if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str) ||
+        !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str) ||
+        !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str)
+                  : make_x_map(&F.tm_dq, dqacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                               (int64_t)nk * d->B, d->H, d->Lq, d->D, part_str, 128,
+                               std::min(dpad(d->D), 32))))
+      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for the output maps");
     evo::BwdFusedArgs& fa = F.args;
     memset(&fa, 0, sizeof(fa));
     fa.B = (int)d->B; fa.H = d->H; fa.Lq = d->Lq; fa.Lk = d->Lk; fa.D = d->D;
@@ -481,11 +495,14 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dq = (__nv_bfloat16*)dq; fa.q_sb = d->q_str[0]; fa.q_sh = d->q_str[1]; fa.q_sl = d->q_str[2];
     fa.dq_acc = dqacc;
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
+    static const bool dbg_timing_b = getenv("EVO_DEBUG_TIMING") != nullptr;
+    fa.dbg = dbg_timing_b ? evo::fwd_debug_ptr() : nullptr;
     if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
     ++nl;
     if (dqacc) {
       evo::ConvertArgs ca{};
       ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
+      ca.nparts = nk; ca.part_stride = (int64_t)d->B * d->H * d->Lq * d->D;
       ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
       if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
       ++nl;
@@ -520,6 +537,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (dqacc) {
     evo::ConvertArgs ca{};
     ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
+    ca.nparts = 1; ca.part_stride = 0;
     ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
     if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
     ++nl;

@@ -25,8 +25,9 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
     const int64_t bh = r / Lq_pad;
     const int h = (int)(bh % a.H);
     const int64_t b = bh / a.H;
+    const float sgn = a.negate ? -1.f : 1.f;
     if (q >= a.Lq) {  // padding rows of the [B*H][Lq_pad] vectors: inert
-      if (!F32) a.lse2[r] = INFINITY;
+      if (!F32) a.lse2[r] = sgn * INFINITY;
       a.Dvec[r] = 0.f;
       continue;
     }
@@ -91,10 +92,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
         }
       }
     }
-    a.Dvec[r] = Dq;
+    a.Dvec[r] = sgn * Dq;
     if (!F32) {
       const float l = a.lse[bh * a.Lq + q];
-      a.lse2[r] = l == -INFINITY ? INFINITY : l * kLog2e;  // no kept key -> P = 0
+      a.lse2[r] = sgn * (l == -INFINITY ? INFINITY : l * kLog2e);  // no kept key -> P = 0
     }
   }
 }
@@ -639,8 +640,14 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
     const int64_t bh = r / a.Lq;
     const int h = (int)(bh % a.H);
     const int64_t b = bh / a.H;
-    const float4 x = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0);
-    const float4 y = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0 + 4);
+    float4 x = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0);
+    float4 y = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0 + 4);
+    for (int p = 1; p < a.nparts; ++p) {
+      const float4 x2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + r * a.D + d0);
+      const float4 y2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + r * a.D + d0 + 4);
+      x.x += x2.x; x.y += x2.y; x.z += x2.z; x.w += x2.w;
+      y.x += y2.x; y.y += y2.y; y.z += y2.z; y.w += y2.w;
+    }
     uint4 st;
     st.x = pack_bf16(x.x * a.scale, x.y * a.scale);
     st.y = pack_bf16(x.z * a.scale, x.w * a.scale);

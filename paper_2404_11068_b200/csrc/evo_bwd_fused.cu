@@ -4,23 +4,27 @@
 // Same arithmetic as evo_bwd.cu's bwd_main + bwd_bias (SPEC.md L168
 // recompute backward; dbias = Σ_b dS over the broadcast axis, PAPER.md L294 / north star), but
 // the probabilities are recomputed ONCE: the CTA loops over its batch rows and, for each, over
-// 64-query sub-tiles, and accumulates Σ_b dSᵀ for its key tile in TMEM (fp32, read-modify-write
+// 32-query sub-tiles, and accumulates Σ_b dSᵀ for its key tile in TMEM (fp32, read-modify-write
 // by the owning thread), so the separate dbias pass and its second recompute disappear.
 //
-// Roles (320 threads): warps 0-7 compute (thread = key row k = TMEM lane, warp>>2 = which 32
-// queries of the 64-query sub-tile), warp 8 lane 0 issues tcgen05.mma, warp 9 lane 0 issues TMA.
-// Per sub-tile j (queries q0..q0+63 of batch row b):
-//   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 64 queries)  -> TMEM
+// Roles (352 threads): two compute warpgroups (warps 0-3, 4-7) take alternate sub-tiles
+// (ping-pong: one group's exp/ALU work covers the other's hand-offs and drains); warp 8 lane 0
+// issues the Sᵀ/dPᵀ MMAs, warp 10 lane 0 the dV/dK/dQ MMAs, warp 9 lane 0 the TMA loads.  Thread = key row k = TMEM lane.
+// Per sub-tile j (queries q0..q0+31 of batch row b), group g = j & 1:
+//   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 32 queries) -> TMEM slot g
 //   compute:  Pᵀ = exp2(Sᵀ·scale·log2e + biasᵀ·log2e − lse2), dSᵀ = Pᵀ⊙(dPᵀ − D)
-//             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ, dSᵀ -> smem bf16 (SW128, K-major)
-//   MMA:      dV_b += Pᵀ·dA_j, dK_b += dSᵀ·Q_j;  after both halves of a 128-query tile:
-//             dQ_part = dS·K_b (A = the dSᵀ tile read MN-major)
-// The next sub-tile's Sᵀ/dPᵀ MMAs are issued as soon as the compute warps have pulled the
-// current ones into registers, so the tensor core runs under the exp/ALU work.
+//             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ -> smem slot g, dSᵀ -> block (j & 3) of the tile
+//   MMA:      dV_b += Pᵀ·dA_j, dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a 128-query tile:
+//             dQ_part = dS·K_b (A = the tile's dSᵀ blocks read MN-major)
+// Group 0 also drains: at the first sub-tile of a query tile the previous tile's dQ part, at a
+// new batch row dK/dV, through swizzled staging tiles and TMA stores.
+// The issuer runs Sᵀ/dPᵀ ahead (one sub-tile per group), so before overwriting its Pᵀ slot a
+// group waits for dV/dK(j-2) (bar_mm) and, at its first sub-tile of a tile, for the previous
+// tile's dQ MMA (bar_dq), the last reader of the dSᵀ blocks.
 //
-// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | Sᵀ 64 | dPᵀ 64 | dV DP | dK DP | dQ DP
-// SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 stages |
-//       Q,dA x2 stages | Pᵀ 16 KB | dSᵀ 32 KB (one 128-query tile) | lse2/D x2 | barriers
+// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | 2 x (Sᵀ 32 | dPᵀ 32) | dV DP | dK DP | dQ DP
+// SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 |
+//       Q,dA x2 | Pᵀ x2 (8 KB) | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
 #include "evo_kernels.cuh"
 
 namespace evo {
@@ -29,26 +33,35 @@ template <int DP, bool BIAS>
 struct FusedCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
   static constexpr uint32_t kTile = 128 * kRowBytes;  // one 128-row Q/K/V/dA tile
-  // resident biasᵀ for Lq_pad <= 256 (<= 128 at DP = 64: bwd_fused_supported's TMEM rule)
-  static constexpr uint32_t kBiasMax = BIAS ? 128u * (DP == 64 ? 128u : 256u) * 2u : 0u;
+  static constexpr uint32_t kBiasMax = BIAS ? 128u * 256u * 2u : 0u;
   static constexpr uint32_t oBias = 0;
   static constexpr uint32_t oKV = oBias + kBiasMax;      // stage s: K at +s*2*kTile, V +kTile
   static constexpr uint32_t oQA = oKV + 4 * kTile;       // stage s: Q at +s*2*kTile, dA +kTile
-  static constexpr uint32_t oP = oQA + 4 * kTile;        // 16 KB
-  static constexpr uint32_t oDS = oP + 16384;            // 32 KB (2 x 64-query halves)
+  static constexpr uint32_t oP = oQA + 4 * kTile;        // 2 x 8 KB  ([128 k][32 q], SW64)
+  static constexpr uint32_t oDS = oP + 16384;            // 4 x 8 KB  (one 128-query tile)
   static constexpr uint32_t oVec = oDS + 32768;          // 2 x (lse2[128], D[128]) fp32
-  static constexpr uint32_t oBar = oVec + 2048;
+  static constexpr uint32_t oStK = oVec + 2048;          // staging: dK, dV bf16, dQ bf16|fp32
+  static constexpr uint32_t oStV = oStK + kTile;
+  static constexpr uint32_t oStQ = oStV + kTile;
+  static constexpr uint32_t oBar = oStQ + 128 * DP * 4;
   static constexpr uint32_t kSmem = oBar + 256;
 };
 
+template <int N>
+EVO_DEV void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_ld16(taddr, r);
+  else tmem_ld32(taddr, r);
+}
+
 template <int DP, bool BIAS>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_da,
-                     const BwdFusedArgs a) {
+                     const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
+                     const __grid_constant__ CUtensorMap tm_dv, const BwdFusedArgs a) {
   using C = FusedCfg<DP, BIAS>;
-  constexpr uint32_t kSw = DP == 64 ? kSw128 : (DP == 32 ? kSw64 : kSw32);
-  constexpr uint32_t kHalf = DP / 2;  // d columns per compute-warp half in the drains
+  static_assert(DP == 16 || DP == 32, "fused backward: head dim pad 16 or 32");
+  constexpr uint32_t kSw = DP == 32 ? kSw64 : kSw32;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s0 = smem_u32(smem);
   if (s0 & 1023u) __trap();
@@ -57,12 +70,13 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t bar_in = smem_u32(&bars[2]);       // +8: stage 1   (TMA Q,dA,vec landed)
   const uint32_t bar_kvfree = smem_u32(&bars[4]);   // +8            (MMA done with K,V stage)
   const uint32_t bar_infree = smem_u32(&bars[6]);   // +8            (MMA done with Q,dA stage)
-  const uint32_t bar_sp = smem_u32(&bars[8]);       // Sᵀ, dPᵀ in TMEM
-  const uint32_t bar_sfree = smem_u32(&bars[9]);    // compute pulled Sᵀ, dPᵀ (8 warps)
-  const uint32_t bar_ps = smem_u32(&bars[10]);      // Pᵀ, dSᵀ in smem (8 warps)
-  const uint32_t bar_mm = smem_u32(&bars[11]);      // dV/dK MMAs of a sub-tile done
-  const uint32_t bar_dq = smem_u32(&bars[12]);      // dQ MMA of a query tile done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[14]);
+  const uint32_t bar_sp = smem_u32(&bars[8]);       // +8: group 1   Sᵀ, dPᵀ in TMEM slot
+  const uint32_t bar_sfree = smem_u32(&bars[10]);   // +8            group pulled its slot (4 warps)
+  const uint32_t bar_ps = smem_u32(&bars[12]);      // +8            Pᵀ, dSᵀ in smem (4 warps)
+  const uint32_t bar_dq = smem_u32(&bars[14]);      // dQ MMA of a query tile (and all before) done
+  const uint32_t bar_dkvfree = smem_u32(&bars[15]); // group 0 pulled a finished dK/dV (4 warps)
+  const uint32_t bar_mm = smem_u32(&bars[16]);      // +8: group 1   dV/dK of its sub-tile done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[18]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
@@ -74,7 +88,9 @@ __global__ void __launch_bounds__(320, 1)
   const int b0 = c * a.chunk;
   const int nb = min(a.B - b0, a.chunk);
   if (nb <= 0) return;
-  const int J = nb * nq * 2;  // sub-tiles
+  const int J = nb * nq * 4;  // 32-query sub-tiles
+  unsigned long long* dbg = (a.dbg && blockIdx.x < 4) ? a.dbg + blockIdx.x * 4096 : nullptr;
+#define DBG(i) do { if (dbg) dbg[i] = clock64(); } while (0)
 
   if (w == 0) tmem_alloc<512>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -83,12 +99,13 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(bar_in + 8 * i, 1);
       mbar_init(bar_kvfree + 8 * i, 1);
       mbar_init(bar_infree + 8 * i, 1);
+      mbar_init(bar_sp + 8 * i, 1);
+      mbar_init(bar_sfree + 8 * i, 4);
+      mbar_init(bar_ps + 8 * i, 4);
+      mbar_init(bar_mm + 8 * i, 1);
     }
-    mbar_init(bar_sp, 1);
-    mbar_init(bar_sfree, 8);
-    mbar_init(bar_ps, 8);
-    mbar_init(bar_mm, 1);
     mbar_init(bar_dq, 1);
+    mbar_init(bar_dkvfree, 4);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -96,8 +113,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t cb = BIAS ? (uint32_t)Lq_pad : 0u;
-  const uint32_t tDB = tmem, tSt = tmem + cb, tdPt = tSt + 64, tdV = tSt + 128, tdK = tdV + DP,
-                 tdQ = tdK + DP;
+  const uint32_t tDB = tmem, tS0 = tmem + cb, tdV = tS0 + 128, tdK = tdV + DP, tdQ = tdK + DP;
 
   if (w == 9) {
     // ------------------------------------------------------------------ TMA producer
@@ -130,68 +146,97 @@ __global__ void __launch_bounds__(320, 1)
   } else if (w == 8) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, 0, 0);   // Sᵀ, dPᵀ
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 32, 0, 0);   // Sᵀ, dPᵀ
+      // Sᵀ/dPᵀ of sub-tile i+2 starts as soon as its group has pulled sub-tile i out of the TMEM
+      // slot (so it runs while that group computes i); dV/dK of sub-tile i once its Pᵀ/dSᵀ are
+      // in smem.  Per group sfree(i) < ps(i) < sfree(i+2), and the two groups run half a period
+      // apart, so this fixed blocking order never waits on an event that a later step produces.
+      auto issue_s = [&](int j, int bi, int t, int s) {
+        const int T = bi * nq + t, st = T & 1, kvs = bi & 1, g = j & 1;
+        if (s == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
+        if (s == 0 && t == 0) mbar_wait(bar_kv + 8 * kvs, (bi >> 1) & 1);
+        if (j < 256) DBG(2048 + j * 4 + 0);
+        tc_fence_after();
+        const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
+        const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + s * 32 * C::kRowBytes;
+        const uint32_t tS = tS0 + g * 64, tdP = tS + 32;
+#pragma unroll
+        for (int kk = 0; kk < DP / 16; ++kk)
+          umma_bf16(tS, make_sdesc(kb + kk * 32, 16, 8 * C::kRowBytes, kSw),
+                    make_sdesc(qb + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DP / 16; ++kk)
+          umma_bf16(tdP, make_sdesc(kb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw),
+                    make_sdesc(qb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s,
+                    kk > 0);
+        umma_commit(bar_sp + 8 * g);
+      };
+      auto advance = [&](int& bi, int& t, int& s) {
+        if (++s == 4) {
+          s = 0;
+          if (++t == nq) { t = 0; ++bi; }
+        }
+      };
+      int sbi = 0, stt = 0, sss = 0;
+      for (int j = 0; j < J; ++j) {
+        if (j >= 2) mbar_wait(bar_sfree + 8 * (j & 1), ((j - 2) >> 1) & 1);
+        issue_s(j, sbi, stt, sss);
+        advance(sbi, stt, sss);
+      }
+    }
+  } else if (w == 10) {
+    // ------------------------------------------------------------------ gradient-MMA issuer
+    // dV/dK of sub-tile i once its Pᵀ/dSᵀ are in smem; the dQ part after a tile's 4th.  A
+    // separate thread from the Sᵀ issuer, so neither stream waits on the other's events.
+    if (lane == 0) {
       constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, 0, 1);  // dV, dK (B MN-major)
       constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, 1, 1);   // dQ (A, B MN-major)
-      for (int j = 0; j <= J; ++j) {
-        if (j < J) {
-          const int bi = j / (2 * nq), t = (j >> 1) % nq, sub = j & 1, T = j >> 1;
-          const int st = T & 1, kvs = bi & 1;
-          if (sub == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
-          if (sub == 0 && t == 0) mbar_wait(bar_kv + 8 * kvs, (bi >> 1) & 1);
-          if (j > 0) mbar_wait(bar_sfree, (j - 1) & 1);
-          tc_fence_after();
+      int dbi = 0, dtt = 0, dss = 0;  // coordinates of sub-tile i
+      for (int i = 0; i < J; ++i) {
+        const int g = i & 1;
+        const int T = dbi * nq + dtt, st = T & 1, kvs = dbi & 1;
+        mbar_wait(bar_ps + 8 * g, (i >> 1) & 1);
+        // the first sub-tile of a new batch row overwrites dK/dV: group 0 must have pulled them
+        if (dtt == 0 && dss == 0 && dbi > 0) mbar_wait(bar_dkvfree, (dbi - 1) & 1);
+        if (i < 256) DBG(2048 + i * 4 + 1);
+        tc_fence_after();
+        const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
+        const uint32_t ab = qb + C::kTile;
+        const uint32_t pb = s0 + C::oP + g * 8192, db = s0 + C::oDS + dss * 8192;
+        const uint32_t acc0 = (dtt > 0 || dss > 0) ? 1u : 0u;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)  // dV += Pᵀ·dA (K = 32 queries)
+          umma_bf16(tdV, make_sdesc(pb + kk * 32, 16, 512, kSw64),
+                    make_sdesc(ab + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
+                    idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)  // dK += dSᵀ·Q
+          umma_bf16(tdK, make_sdesc(db + kk * 32, 16, 512, kSw64),
+                    make_sdesc(qb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
+                    idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
+        umma_commit(bar_mm + 8 * g);
+        if (dss == 3) {  // the tile's 4 dSᵀ blocks are complete: dQ part = dS·K
           const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
-          const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + sub * 64 * C::kRowBytes;
 #pragma unroll
-          for (int kk = 0; kk < DP / 16; ++kk)
-            umma_bf16(tSt, make_sdesc(kb + kk * 32, 16, 8 * C::kRowBytes, kSw),
-                      make_sdesc(qb + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s, kk > 0);
-#pragma unroll
-          for (int kk = 0; kk < DP / 16; ++kk)
-            umma_bf16(tdPt, make_sdesc(kb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw),
-                      make_sdesc(qb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s,
-                      kk > 0);
-          umma_commit(bar_sp);
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tdQ, make_sdesc(s0 + C::oDS + kk * 1024, 8192, 512, kSw64),
+                      make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
+                      idesc_q, kk > 0 ? 1u : 0u);
+          umma_commit(bar_dq);
+          // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the groups' hand-offs;
+          // dV/dK/dQ: this thread) is done once these commits land
+          umma_commit(bar_infree + 8 * st);
+          if (dtt == nq - 1) umma_commit(bar_kvfree + 8 * kvs);
         }
-        if (j > 0) {
-          const int i = j - 1;
-          const int bi = i / (2 * nq), t = (i >> 1) % nq, sub = i & 1, T = i >> 1;
-          const int st = T & 1, kvs = bi & 1;
-          mbar_wait(bar_ps, i & 1);
-          tc_fence_after();
-          const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + sub * 64 * C::kRowBytes;
-          const uint32_t ab = qb + C::kTile;
-          const uint32_t pb = s0 + C::oP, db = s0 + C::oDS + sub * 16384;
-          const uint32_t acc0 = (t > 0 || sub > 0) ? 1u : 0u;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // dV += Pᵀ·dA (K = 64 queries)
-            umma_bf16(tdV, make_sdesc(pb + kk * 32, 16, 1024, kSw128),
-                      make_sdesc(ab + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
-                      idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // dK += dSᵀ·Q
-            umma_bf16(tdK, make_sdesc(db + kk * 32, 16, 1024, kSw128),
-                      make_sdesc(qb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
-                      idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
-          umma_commit(bar_mm);
-          if (sub == 1) {  // both halves of the query tile are in the dSᵀ buffer: dQ part
-            const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16(tdQ, make_sdesc(s0 + C::oDS + kk * 2048, 16384, 1024, kSw128),
-                        make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
-                        idesc_q, kk > 0 ? 1u : 0u);
-            umma_commit(bar_dq);
-            umma_commit(bar_infree + 8 * st);
-            if (t == nq - 1) umma_commit(bar_kvfree + 8 * kvs);
-          }
+        if (++dss == 4) {
+          dss = 0;
+          if (++dtt == nq) { dtt = 0; ++dbi; }
         }
       }
     }
   } else {
-    // ------------------------------------------------------------------ compute warps 0-7
-    const int qd = w & 3, hh = w >> 2;
+    // ------------------------------------------------------------------ compute warpgroups
+    const int g = w >> 2, qd = w & 3;
     const int row = qd * 32 + lane;  // key row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
     const uint32_t RB = (uint32_t)Lq_pad * 2;  // resident biasᵀ row bytes
@@ -247,48 +292,113 @@ __global__ void __launch_bounds__(320, 1)
 
     const uint64_t sl2 = f2_pack(a.scale_log2, a.scale_log2);
     const uint64_t l2e2 = f2_pack(kLog2e, kLog2e);
-    bool keep = false;
     const int kglob = k0 + row;
-    for (int j = 0; j < J; ++j) {
-      const int bi = j / (2 * nq), t = (j >> 1) % nq, sub = j & 1, T = j >> 1;
+    // ---- drains (group 0): TMEM rows -> swizzled staging tiles -> one thread's TMA stores
+    constexpr uint32_t kRbB = DP * 2;  // bf16 staging row bytes (= the x-map swizzle span)
+    constexpr uint32_t kRbF = DP * 4;  // fp32 staging row bytes
+    auto stage_bf16 = [&](uint32_t base, const uint32_t (&r)[DP], float mul) {
+#pragma unroll
+      for (int i = 0; i < DP / 8; ++i)
+        st_shared_v4(base + swz_offset(row, i, kRbB),
+                     pack_bf16(__uint_as_float(r[8 * i]) * mul, __uint_as_float(r[8 * i + 1]) * mul),
+                     pack_bf16(__uint_as_float(r[8 * i + 2]) * mul, __uint_as_float(r[8 * i + 3]) * mul),
+                     pack_bf16(__uint_as_float(r[8 * i + 4]) * mul, __uint_as_float(r[8 * i + 5]) * mul),
+                     pack_bf16(__uint_as_float(r[8 * i + 6]) * mul, __uint_as_float(r[8 * i + 7]) * mul));
+    };
+    auto stage_f32 = [&](uint32_t base, const uint32_t (&r)[DP]) {
+#pragma unroll
+      for (int i = 0; i < DP / 4; ++i)
+        st_shared_v4(base + swz_offset(row, i, kRbF), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                     r[4 * i + 3]);
+    };
+    // dQ part of (bq, query tile at q0) and, if kv, dK/dV of batch row bk.  Called after the
+    // bar_dq wait (all MMAs up to that tile's dQ complete).  dK/dV are pulled first and released
+    // on bar_dkvfree (the next batch row's first dV/dK MMA overwrites them); the dQ part stays
+    // valid until the next tile's dQ MMA, which waits for this group's next hand-off.
+    auto drain = [&](int bq, int q0, bool kv, int bk, bool release_kv) {
+      if (tid == 0) bulk_wait_group_read0();  // the previous drain's stores left the staging
+      named_bar_sync(2, 128);
+      uint32_t r[DP];
+      if (kv) {
+        tmem_ld_cols(tdK + lane_base, r);
+        tmem_wait_ld();
+        stage_bf16(s0 + C::oStK, r, a.scale);
+        tmem_ld_cols(tdV + lane_base, r);
+        tmem_wait_ld();
+        if (release_kv) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_dkvfree);
+        }
+        stage_bf16(s0 + C::oStV, r, 1.f);
+      }
+      tmem_ld_cols(tdQ + lane_base, r);
+      tmem_wait_ld();
+      if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
+      else stage_f32(s0 + C::oStQ, r);
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (tid == 0) {
+        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
+        if (kv) {
+          tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
+          tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
+        }
+        bulk_commit_group();
+      }
+    };
+    // hard-mask bit of this thread's key for batch row b (prefetched one batch row ahead)
+    auto load_keep = [&](int b) -> uint32_t {
+      if (kglob >= a.Lk || b >= a.B) return 0u;
+      return a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kglob * a.mask_s1] : 1u;
+    };
+    uint32_t keep_next = load_keep(b0);
+    bool keep = false;
+    int bi = 0, t = 0, s = g;  // this group's sub-tiles: j = g, g+2, ...; j = ((bi*nq)+t)*4 + s
+    for (int j = g; j < J; j += 2) {
+      const int T = bi * nq + t;
       const int st = T & 1;
       const int b = b0 + bi;
-      if (sub == 0 && t == 0) {
-        keep = kglob < a.Lk;
-        if (keep && a.mask) keep = a.mask[(int64_t)b * a.mask_s0 + (int64_t)kglob * a.mask_s1] != 0;
+      if (s == g && t == 0) {
+        keep = keep_next != 0u;
+        keep_next = load_keep(b + 1);
       }
-      mbar_wait(bar_sp, j & 1);
+      const bool rec = tid == 0 && j < 256;
+      if (rec) DBG(j * 8 + 0);
+      mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
+      if (rec) DBG(j * 8 + 1);
       tc_fence_after();
       uint32_t rs[32], rd[32];
-      tmem_ld32(tSt + lane_base + hh * 32, rs);
-      tmem_ld32(tdPt + lane_base + hh * 32, rd);
+      {
+        const uint32_t tS = tS0 + g * 64;
+        tmem_ld32(tS + lane_base, rs);
+        tmem_ld32(tS + 32 + lane_base, rd);
+      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_sfree);
+      if (lane == 0) mbar_arrive(bar_sfree + 8 * g);
+      if (rec) DBG(j * 8 + 2);
       mbar_wait(bar_in + 8 * st, (T >> 1) & 1);  // lse2 / D of this query tile visible
-      const uint32_t vbase = s0 + C::oVec + st * 1024 + (sub * 64 + hh * 32) * 4;
-      const int qcol = t * 128 + sub * 64 + hh * 32;  // first query of this thread's 32
+      const uint32_t vbase = s0 + C::oVec + st * 1024 + s * 32 * 4;
+      const int qcol = t * 128 + s * 32;  // first query of this sub-tile
       uint32_t pk[16], dk2[16];
       float ds[32];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {  // 8 queries per group
-        const uint4 l0 = ld_shared_v4(vbase + g * 32), l1 = ld_shared_v4(vbase + g * 32 + 16);
-        const uint4 d0 = ld_shared_v4(vbase + 512 + g * 32), d1 = ld_shared_v4(vbase + 512 + g * 32 + 16);
-        const uint32_t nl[8] = {l0.x ^ 0x80000000u, l0.y ^ 0x80000000u, l0.z ^ 0x80000000u,
-                                l0.w ^ 0x80000000u, l1.x ^ 0x80000000u, l1.y ^ 0x80000000u,
-                                l1.z ^ 0x80000000u, l1.w ^ 0x80000000u};
-        const uint32_t nd[8] = {d0.x ^ 0x80000000u, d0.y ^ 0x80000000u, d0.z ^ 0x80000000u,
-                                d0.w ^ 0x80000000u, d1.x ^ 0x80000000u, d1.y ^ 0x80000000u,
-                                d1.z ^ 0x80000000u, d1.w ^ 0x80000000u};
+      for (int gq = 0; gq < 4; ++gq) {  // 8 queries per group
+        // the vectors arrive negated: -lse·log2e (-inf for rows without a kept key), -D
+        const uint4 l0 = ld_shared_v4(vbase + gq * 32), l1 = ld_shared_v4(vbase + gq * 32 + 16);
+        const uint4 d0 = ld_shared_v4(vbase + 512 + gq * 32), d1 = ld_shared_v4(vbase + 512 + gq * 32 + 16);
+        const uint32_t nl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        const uint32_t nd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
         uint32_t bu[4] = {0, 0, 0, 0};
         if (BIAS) {
-          const uint4 bv = ld_shared_v4(sBias + row * RB + (((uint32_t)(qcol >> 3) + g) ^ (row & 7)) * 16);
+          const uint4 bv = ld_shared_v4(sBias + row * RB + (((uint32_t)(qcol >> 3) + gq) ^ (row & 7)) * 16);
           bu[0] = bv.x; bu[1] = bv.y; bu[2] = bv.z; bu[3] = bv.w;
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int i = g * 8 + 2 * e;
+          const int i = gq * 8 + 2 * e;
           const uint64_t nl2 = ((uint64_t)nl[2 * e + 1] << 32) | nl[2 * e];
           const uint64_t nd2 = ((uint64_t)nd[2 * e + 1] << 32) | nd[2 * e];
           uint64_t x = BIAS ? f2_fma(bf16x2_to_f2(bu[e]), l2e2, nl2) : nl2;
@@ -304,7 +414,7 @@ __global__ void __launch_bounds__(320, 1)
           dk2[i / 2] = pack_bf16(ds[i], ds[i + 1]);
         }
       }
-      if (BIAS) {  // Σ_b dSᵀ in TMEM (this thread's lane, its 32 query columns)
+      if (BIAS) {  // Σ_b dSᵀ in TMEM (this thread's lane, this sub-tile's 32 query columns)
         uint32_t acc[32];
         if (bi == 0) {  // first batch row of the chunk initialises the (uninitialised) TMEM
 #pragma unroll
@@ -323,86 +433,20 @@ __global__ void __launch_bounds__(320, 1)
         }
         tmem_st32(tDB + lane_base + qcol, acc);
       }
-      // previous sub-tile's dV/dK MMAs have consumed Pᵀ / dSᵀ (and, at a new batch row, the
-      // dK/dV accumulators are final; at a new query tile, dQ of the previous one is issued)
-      if (j > 0) {
-        mbar_wait(bar_mm, (j - 1) & 1);
-        tc_fence_after();
-        if (sub == 0) {  // dQ part of query tile T-1 (TMEM lane = query row)
-          mbar_wait(bar_dq, (T - 1) & 1);
-          tc_fence_after();
-          const int tp = (T - 1) % nq, bp = b0 + (T - 1) / nq;
-          const int q = tp * 128 + row;
-          uint32_t r[kHalf];
-          if constexpr (kHalf == 8) tmem_ld8(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(r));
-          else if constexpr (kHalf == 16) tmem_ld16(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(r));
-          else tmem_ld32(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(r));
-          tmem_wait_ld();
-          if (q < a.Lq) {
-#pragma unroll
-            for (int e = 0; e < (int)kHalf; e += 8) {
-              const int d0 = hh * kHalf + e;
-              if (d0 >= a.D) break;
-              if (nk == 1) {
-                uint4 o;
-                o.x = pack_bf16(__uint_as_float(r[e]) * a.scale, __uint_as_float(r[e + 1]) * a.scale);
-                o.y = pack_bf16(__uint_as_float(r[e + 2]) * a.scale, __uint_as_float(r[e + 3]) * a.scale);
-                o.z = pack_bf16(__uint_as_float(r[e + 4]) * a.scale, __uint_as_float(r[e + 5]) * a.scale);
-                o.w = pack_bf16(__uint_as_float(r[e + 6]) * a.scale, __uint_as_float(r[e + 7]) * a.scale);
-                *reinterpret_cast<uint4*>(a.dq + (int64_t)bp * a.q_sb + (int64_t)h * a.q_sh +
-                                          (int64_t)q * a.q_sl + d0) = o;
-              } else {
-                float4* dst = reinterpret_cast<float4*>(a.dq_acc + (((int64_t)bp * a.H + h) * a.Lq + q) * a.D + d0);
-                atomicAdd(dst, make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
-                                           __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3])));
-                atomicAdd(dst + 1, make_float4(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]),
-                                               __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7])));
-              }
-            }
-          }
-          if (t == 0) {  // dK, dV of the previous batch row are complete
-            const int bprev = b - 1;
-            uint32_t rk[kHalf], rv[kHalf];
-            if constexpr (kHalf == 8) {
-              tmem_ld8(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(rk));
-              tmem_ld8(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(rv));
-            } else if constexpr (kHalf == 16) {
-              tmem_ld16(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(rk));
-              tmem_ld16(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(rv));
-            } else {
-              tmem_ld32(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(rk));
-              tmem_ld32(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(rv));
-            }
-            tmem_wait_ld();
-            if (kglob < a.Lk) {
-#pragma unroll
-              for (int e = 0; e < (int)kHalf; e += 8) {
-                const int d0 = hh * kHalf + e;
-                if (d0 >= a.D) break;
-                uint4 x, y;
-                x.x = pack_bf16(__uint_as_float(rk[e]) * a.scale, __uint_as_float(rk[e + 1]) * a.scale);
-                x.y = pack_bf16(__uint_as_float(rk[e + 2]) * a.scale, __uint_as_float(rk[e + 3]) * a.scale);
-                x.z = pack_bf16(__uint_as_float(rk[e + 4]) * a.scale, __uint_as_float(rk[e + 5]) * a.scale);
-                x.w = pack_bf16(__uint_as_float(rk[e + 6]) * a.scale, __uint_as_float(rk[e + 7]) * a.scale);
-                y.x = pack_bf16(__uint_as_float(rv[e]), __uint_as_float(rv[e + 1]));
-                y.y = pack_bf16(__uint_as_float(rv[e + 2]), __uint_as_float(rv[e + 3]));
-                y.z = pack_bf16(__uint_as_float(rv[e + 4]), __uint_as_float(rv[e + 5]));
-                y.w = pack_bf16(__uint_as_float(rv[e + 6]), __uint_as_float(rv[e + 7]));
-                *reinterpret_cast<uint4*>(a.dk + (int64_t)bprev * a.k_sb + (int64_t)h * a.k_sh +
-                                          (int64_t)kglob * a.k_sl + d0) = x;
-                *reinterpret_cast<uint4*>(a.dv + (int64_t)bprev * a.v_sb + (int64_t)h * a.v_sh +
-                                          (int64_t)kglob * a.v_sl + d0) = y;
-              }
-            }
-          }
-        }
-      }
-      // Pᵀ and dSᵀ rows (this thread's key row, its 32 queries = 4 x 16-B chunks, SW128)
+      if (rec) DBG(j * 8 + 3);
+      // before overwriting: Pᵀ slot g is read by dV(j-2); the dSᵀ blocks of the previous tile by
+      // its dQ MMA (each group checks at its first sub-tile of a tile)
+      if (j >= 2) mbar_wait(bar_mm + 8 * g, ((j - 2) >> 1) & 1);
+      if (s == g && T > 0) mbar_wait(bar_dq, (T - 1) & 1);
+      if (rec) DBG(j * 8 + 4);
+      tc_fence_after();
+      const bool drain_now = g == 0 && s == 0 && j > 0;
+      // Pᵀ (slot g) and dSᵀ (block s) rows: this thread's key row, 32 queries = 4 x 16 B, SW64
       {
-        const uint32_t pb = s0 + C::oP, db = s0 + C::oDS + sub * 16384;
+        const uint32_t pb = s0 + C::oP + g * 8192, db = s0 + C::oDS + s * 8192;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t off = swz_offset(row, hh * 4 + e, 128);
+          const uint32_t off = swz_offset(row, e, 64);
           st_shared_v4(pb + off, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
           st_shared_v4(db + off, dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
         }
@@ -411,73 +455,29 @@ __global__ void __launch_bounds__(320, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_ps);
-    }
-    // ---- tail: last dQ part, last dK/dV, then this chunk's Σ_b dSᵀ
-    mbar_wait(bar_mm, (J - 1) & 1);
-    mbar_wait(bar_dq, ((J >> 1) - 1) & 1);
-    tc_fence_after();
-    {
-      const int Tl = (J >> 1) - 1;
-      const int tp = Tl % nq, bp = b0 + Tl / nq;
-      const int q = tp * 128 + row;
-      uint32_t r[kHalf], rk[kHalf], rv[kHalf];
-      if constexpr (kHalf == 8) {
-        tmem_ld8(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(r));
-        tmem_ld8(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(rk));
-        tmem_ld8(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[8]>(rv));
-      } else if constexpr (kHalf == 16) {
-        tmem_ld16(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(r));
-        tmem_ld16(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(rk));
-        tmem_ld16(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[16]>(rv));
-      } else {
-        tmem_ld32(tdQ + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(r));
-        tmem_ld32(tdK + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(rk));
-        tmem_ld32(tdV + lane_base + hh * kHalf, *reinterpret_cast<uint32_t(*)[32]>(rv));
+      if (lane == 0) mbar_arrive(bar_ps + 8 * g);
+      if (rec) DBG(j * 8 + 5);
+      if (drain_now) {  // group 0: the previous query tile's dQ part (+ dK/dV at a new row)
+        const int Tp = T - 1;
+        drain(b0 + Tp / nq, (Tp % nq) * 128, t == 0, b - 1, true);
       }
-      tmem_wait_ld();
-#pragma unroll
-      for (int e = 0; e < (int)kHalf; e += 8) {
-        const int d0 = hh * kHalf + e;
-        if (d0 >= a.D) break;
-        if (q < a.Lq) {
-          if (nk == 1) {
-            uint4 o;
-            o.x = pack_bf16(__uint_as_float(r[e]) * a.scale, __uint_as_float(r[e + 1]) * a.scale);
-            o.y = pack_bf16(__uint_as_float(r[e + 2]) * a.scale, __uint_as_float(r[e + 3]) * a.scale);
-            o.z = pack_bf16(__uint_as_float(r[e + 4]) * a.scale, __uint_as_float(r[e + 5]) * a.scale);
-            o.w = pack_bf16(__uint_as_float(r[e + 6]) * a.scale, __uint_as_float(r[e + 7]) * a.scale);
-            *reinterpret_cast<uint4*>(a.dq + (int64_t)bp * a.q_sb + (int64_t)h * a.q_sh +
-                                      (int64_t)q * a.q_sl + d0) = o;
-          } else {
-            float4* dst = reinterpret_cast<float4*>(a.dq_acc + (((int64_t)bp * a.H + h) * a.Lq + q) * a.D + d0);
-            atomicAdd(dst, make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
-                                       __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3])));
-            atomicAdd(dst + 1, make_float4(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]),
-                                           __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7])));
-          }
-        }
-        if (kglob < a.Lk) {
-          const int bl = b0 + nb - 1;
-          uint4 x, y;
-          x.x = pack_bf16(__uint_as_float(rk[e]) * a.scale, __uint_as_float(rk[e + 1]) * a.scale);
-          x.y = pack_bf16(__uint_as_float(rk[e + 2]) * a.scale, __uint_as_float(rk[e + 3]) * a.scale);
-          x.z = pack_bf16(__uint_as_float(rk[e + 4]) * a.scale, __uint_as_float(rk[e + 5]) * a.scale);
-          x.w = pack_bf16(__uint_as_float(rk[e + 6]) * a.scale, __uint_as_float(rk[e + 7]) * a.scale);
-          y.x = pack_bf16(__uint_as_float(rv[e]), __uint_as_float(rv[e + 1]));
-          y.y = pack_bf16(__uint_as_float(rv[e + 2]), __uint_as_float(rv[e + 3]));
-          y.z = pack_bf16(__uint_as_float(rv[e + 4]), __uint_as_float(rv[e + 5]));
-          y.w = pack_bf16(__uint_as_float(rv[e + 6]), __uint_as_float(rv[e + 7]));
-          *reinterpret_cast<uint4*>(a.dk + (int64_t)bl * a.k_sb + (int64_t)h * a.k_sh +
-                                    (int64_t)kglob * a.k_sl + d0) = x;
-          *reinterpret_cast<uint4*>(a.dv + (int64_t)bl * a.v_sb + (int64_t)h * a.v_sh +
-                                    (int64_t)kglob * a.v_sl + d0) = y;
-        }
+      s += 2;
+      if (s >= 4) {
+        s -= 4;
+        if (++t == nq) { t = 0; ++bi; }
       }
     }
-    if (BIAS) {  // partial[c][h][q][k0 + row] for all padded q (32-column blocks alternate by hh)
+    // ---- tail (group 0): last dQ part and last dK/dV; then both groups write Σ_b dSᵀ
+    if (g == 0) {
+      const int Tl = (J >> 2) - 1;
+      mbar_wait(bar_dq, Tl & 1);
+      tc_fence_after();
+      drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false);
+      if (tid == 0) bulk_wait_group0();
+    }
+    if (BIAS) {  // partial[c][h][q][k0 + row]: this group's 32-query column blocks
       float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
-      for (int cbk = hh; cbk < Lq_pad / 32; cbk += 2) {
+      for (int cbk = g; cbk < Lq_pad / 32; cbk += 2) {
         uint32_t acc[32];
         tmem_ld32(tDB + lane_base + cbk * 32, acc);
         tmem_wait_ld();
@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   }
+#undef DBG
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
@@ -500,7 +501,8 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
-  kern<<<(unsigned)grid, 320, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.args);
+  kern<<<(unsigned)grid, 352, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
+                                          L.tm_dv, L.args);
   return cudaGetLastError();
 }
 
@@ -509,7 +511,6 @@ cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias,
   if (DP == dp && (has_bias != 0) == bb) return launch_bwd_fused_t<dp, bb>(L, st);
   EVO_FUSED_CASE(16, false) EVO_FUSED_CASE(16, true)
   EVO_FUSED_CASE(32, false) EVO_FUSED_CASE(32, true)
-  EVO_FUSED_CASE(64, false) EVO_FUSED_CASE(64, true)
 #undef EVO_FUSED_CASE
   return cudaErrorInvalidValue;
 }

@@ -56,6 +56,7 @@ struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
   float* lse2;   // lse*log2e, +inf for rows with no kept key (bf16 path) | lse (f32 path)
   float* Dvec;   // Σ_d dO·o
   void* dA;      // [B,H,Lq,D] contiguous dO·sigmoid(g) (NULL when no gate)
+  int negate;    // store -lse2 and -D (the fused backward's operand form)
 };
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st);
 
@@ -124,17 +125,19 @@ struct BwdFusedArgs {
   int64_t v_sb, v_sh, v_sl;
   __nv_bfloat16* dq;  // direct store when there is a single key tile
   int64_t q_sb, q_sh, q_sl;
-  float* dq_acc;      // [B,H,Lq,D] fp32 accumulator otherwise
+  float* dq_acc;      // otherwise [nk][B,H,Lq,D] fp32: key tile kt's dQ part (plain stores)
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
+  unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da;
+  CUtensorMap tm_dq, tm_dk, tm_dv;  // output maps (dq: bf16 over dq, or fp32 over the dQ parts)
   BwdFusedArgs args;
 };
 // eligibility + resources of the fused path for head-dim pad DP and padded Lq
 inline bool bwd_fused_supported(int DP, int Lq_pad, bool bias) {
   const int cols = (bias ? Lq_pad : 0) + 128 + 3 * DP;
-  return Lq_pad <= 256 && cols <= 512 && DP >= 16;
+  return Lq_pad <= 256 && cols <= 512 && (DP == 16 || DP == 32);
 }
 inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
   const int groups = H * nk;
@@ -157,10 +160,12 @@ struct ReduceArgs {  // dbias[h,q,k] (bias strides) = Σ_c partial[c][h][q][k]
 };
 cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st);
 
-struct ConvertArgs {  // dq = bf16(scale * dq_acc)
+struct ConvertArgs {  // dq = bf16(scale * Σ_p acc[p])
   int B, H, Lq, D;
   float scale;
   const float* acc;
+  int nparts;
+  int64_t part_stride;  // elements between parts
   __nv_bfloat16* dq;
   int64_t q_sb, q_sh, q_sl;
 };

@@ -1,0 +1,33 @@
+"""Sub-tile timeline of the fused backward (EVO_DEBUG_TIMING=1), CTA 0: compute thread 0 (group
+0, even sub-tiles) and the MMA issuer."""
+import ctypes, os, sys
+os.environ["EVO_DEBUG_TIMING"] = "1"
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import numpy as np, torch
+import bench
+from paper_2404_11068_b200 import evoattn
+dev = torch.device("cuda:0")
+which = sys.argv[1] if len(sys.argv) > 1 else "row"
+for i, (name, B, H, L, bias) in enumerate(bench.MODULES):
+    if name != which: continue
+    t = bench.make_module_inputs(torch, dev, name, B, H, L, bias, seed=100 + i)
+    o, lse = evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
+    for _ in range(3):
+        evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"], t["mask"], t["g"])
+    torch.cuda.synchronize()
+lib = evoattn.load()
+buf = np.zeros(148 * 8 * 32 * 8 + 148 * 64 * 4, dtype=np.uint64)
+lib.evo_debug_fwd_timing(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
+d = buf[:4096].astype(np.int64)
+t0 = d[0]
+print("j  | spwait  spdone  ldone  compdone  dqdone  psarr | MMA: sfree_seen  ps_seen")
+for j in range(0, 40, 2):
+    c = d[j * 8: j * 8 + 6] - t0
+    m = d[2048 + j * 4: 2048 + j * 4 + 2] - t0
+    print(f"{j:2d} | " + " ".join(f"{x:7d}" for x in c) + " | " + " ".join(f"{x:7d}" for x in m))
+c = d[:256 * 8].reshape(256, 8)[::2]
+n = np.count_nonzero(c[:, 5])
+c = c[:n]
+print("median (group 0): sp_wait", np.median(c[:, 1] - c[:, 0]), "ld", np.median(c[:, 2] - c[:, 1]),
+      "compute", np.median(c[:, 3] - c[:, 2]), "store+arrive", np.median(c[:, 5] - c[:, 3]),
+      "period (2 sub-tiles)", np.median(np.diff(c[:, 0])))
