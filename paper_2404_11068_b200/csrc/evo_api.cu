@@ -425,10 +425,14 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   pa.g = g; pa.g_sb = d->g_str[0]; pa.g_sh = d->g_str[1]; pa.g_sl = d->g_str[2]; pa.dg = dg;
   pa.lse = lse; pa.lse2 = lse2; pa.Dvec = dvec; pa.dA = dA;
   pa.negate = W.fused ? 1 : 0;
+  // dA workspace: dense, in the (h, l) order of o's strides so bwd_pre's accesses coalesce
+  const bool o_hfast = d->o_str[1] < d->o_str[2];
+  const int64_t da_str[3] = {(int64_t)d->H * d->Lq * d->D, o_hfast ? d->D : (int64_t)d->Lq * d->D,
+                             o_hfast ? (int64_t)d->H * d->D : d->D};
+  pa.a_sb = da_str[0]; pa.a_sh = da_str[1]; pa.a_sl = da_str[2];
   if ((e = traced(st, "bwd_pre", [&] { return evo::launch_bwd_pre(pa, d->dtype == EVO_F32, st); })) != cudaSuccess) return cuda_fail(e, "bwd_pre");
   ++nl;
   // dA operand: workspace [B,H,Lq,D] contiguous, or dout itself when there is no gate
-  const int64_t da_str[3] = {(int64_t)d->H * d->Lq * d->D, (int64_t)d->Lq * d->D, d->D};
   const void* dA_ptr = d->has_gate ? dA : dout;
   const int64_t* dA_str = d->has_gate ? da_str : d->o_str;
 
@@ -472,7 +476,10 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
     // output maps for the TMA-store drains: dk/dv (bf16, k/v strides); dq (bf16, q strides)
     // when there is one key tile, else the fp32 parts [nk*B][H][Lq][D] (32-column boxes)
-    const int64_t part_str[3] = {(int64_t)d->H * d->Lq * d->D, (int64_t)d->Lq * d->D, d->D};
+    const bool q_hfast = d->q_str[1] < d->q_str[2];  // parts follow dq's (h, l) order
+    const int64_t part_str[3] = {(int64_t)d->H * d->Lq * d->D,
+                                 q_hfast ? d->D : (int64_t)d->Lq * d->D,
+                                 q_hfast ? (int64_t)d->H * d->D : d->D};
     if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str) ||
         !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str) ||
         !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str)
@@ -503,6 +510,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
       evo::ConvertArgs ca{};
       ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
       ca.nparts = nk; ca.part_stride = (int64_t)d->B * d->H * d->Lq * d->D;
+      ca.p_sb = part_str[0]; ca.p_sh = part_str[1]; ca.p_sl = part_str[2];
       ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
       if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
       ++nl;
@@ -537,7 +545,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (dqacc) {
     evo::ConvertArgs ca{};
     ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
-    ca.nparts = 1; ca.part_stride = 0;
+    ca.nparts = 1; ca.part_stride = 0;  // bwd_main's atomic accumulator: [B,H,Lq,D]
+    ca.p_sb = (int64_t)d->H * d->Lq * d->D; ca.p_sh = (int64_t)d->Lq * d->D; ca.p_sl = d->D;
     ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
     if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
     ++nl;

@@ -15,99 +15,111 @@
 namespace evo {
 
 // =============================================================================== bwd_pre
+// CTA per (b, 32 query rows) x all heads.  Rows are visited in the order of the smaller of the
+// (h, l) strides of o, so a warp's 16-byte loads/stores cover consecutive memory; the per-row
+// statistics go through shared memory and leave as coalesced [B*H][Lq_pad] vectors.
 template <bool F32>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
+  constexpr int kHC = 16;  // heads per pass
+  __shared__ float sD[kHC][32], sL[kHC][32];
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
-  const int64_t nrows = (int64_t)a.B * a.H * Lq_pad;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(r % Lq_pad);
-    const int64_t bh = r / Lq_pad;
-    const int h = (int)(bh % a.H);
-    const int64_t b = bh / a.H;
-    const float sgn = a.negate ? -1.f : 1.f;
-    if (q >= a.Lq) {  // padding rows of the [B*H][Lq_pad] vectors: inert
-      if (!F32) a.lse2[r] = sgn * INFINITY;
-      a.Dvec[r] = 0.f;
-      continue;
-    }
-    const int64_t orow = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl;
-    const int64_t grow = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl;
-    const int64_t arow = (bh * a.Lq + q) * a.D;
-    float Dq = 0.f;
-    for (int d0 = 0; d0 < a.D; d0 += 8) {
-      float o8[8], do8[8], g8[8];
-      if (F32) {
-        const float* op = reinterpret_cast<const float*>(a.o) + orow + d0;
-        const float* dp = reinterpret_cast<const float*>(a.dout) + orow + d0;
+  const int nqb = Lq_pad / 32;
+  const int64_t b = blockIdx.x / nqb;
+  const int q0 = (blockIdx.x % nqb) * 32;
+  const bool hfast = a.o_sh < a.o_sl;
+  const float sgn = a.negate ? -1.f : 1.f;
+  for (int h0 = 0; h0 < a.H; h0 += kHC) {
+    const int hc = min(kHC, a.H - h0);
+    for (int r = threadIdx.x; r < 32 * hc; r += blockDim.x) {
+      const int qi = hfast ? r / hc : r % 32, hi = hfast ? r % hc : r / 32;
+      const int q = q0 + qi, h = h0 + hi;
+      float Dq = 0.f, lv = F32 ? 0.f : sgn * INFINITY;  // padding rows: inert
+      if (q < a.Lq) {
+        const int64_t orow = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl;
+        const int64_t grow = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl;
+        const int64_t arow = b * a.a_sb + h * a.a_sh + (int64_t)q * a.a_sl;
+        for (int d0 = 0; d0 < a.D; d0 += 8) {
+          float o8[8], do8[8], g8[8];
+          if (F32) {
+            const float* op = reinterpret_cast<const float*>(a.o) + orow + d0;
+            const float* dp = reinterpret_cast<const float*>(a.dout) + orow + d0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) { o8[e] = op[e]; do8[e] = dp[e]; }
-        if (a.g) {
-          const float* gp = reinterpret_cast<const float*>(a.g) + grow + d0;
+            for (int e = 0; e < 8; ++e) { o8[e] = op[e]; do8[e] = dp[e]; }
+            if (a.g) {
+              const float* gp = reinterpret_cast<const float*>(a.g) + grow + d0;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) g8[e] = gp[e];
+              for (int e = 0; e < 8; ++e) g8[e] = gp[e];
+            }
+          } else {
+            const uint4 ov = *reinterpret_cast<const uint4*>(
+                reinterpret_cast<const __nv_bfloat16*>(a.o) + orow + d0);
+            const uint4 dv = *reinterpret_cast<const uint4*>(
+                reinterpret_cast<const __nv_bfloat16*>(a.dout) + orow + d0);
+            const uint32_t ou[4] = {ov.x, ov.y, ov.z, ov.w}, du[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              o8[2 * e] = bf16_lo(ou[e]); o8[2 * e + 1] = bf16_hi(ou[e]);
+              do8[2 * e] = bf16_lo(du[e]); do8[2 * e + 1] = bf16_hi(du[e]);
+            }
+            if (a.g) {
+              const uint4 gv = *reinterpret_cast<const uint4*>(
+                  reinterpret_cast<const __nv_bfloat16*>(a.g) + grow + d0);
+              const uint32_t gu[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) { g8[2 * e] = bf16_lo(gu[e]); g8[2 * e + 1] = bf16_hi(gu[e]); }
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) Dq = fmaf(do8[e], o8[e], Dq);
+          if (a.g) {
+            float da[8], dg[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float sg = F32 ? 1.f / (1.f + expf(-g8[e])) : 1.f / (1.f + __expf(-g8[e]));
+              da[e] = do8[e] * sg;
+              dg[e] = do8[e] * o8[e] * (1.f - sg);
+            }
+            if (F32) {
+              float* dap = reinterpret_cast<float*>(a.dA) + arow + d0;
+              float* dgp = reinterpret_cast<float*>(a.dg) + grow + d0;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) { dap[e] = da[e]; dgp[e] = dg[e]; }
+            } else {
+              uint4 x, y;
+              x.x = pack_bf16(da[0], da[1]); x.y = pack_bf16(da[2], da[3]);
+              x.z = pack_bf16(da[4], da[5]); x.w = pack_bf16(da[6], da[7]);
+              y.x = pack_bf16(dg[0], dg[1]); y.y = pack_bf16(dg[2], dg[3]);
+              y.z = pack_bf16(dg[4], dg[5]); y.w = pack_bf16(dg[6], dg[7]);
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow + d0) = x;
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dg) + grow + d0) = y;
+            }
+          }
         }
-      } else {
-        const uint4 ov = *reinterpret_cast<const uint4*>(
-            reinterpret_cast<const __nv_bfloat16*>(a.o) + orow + d0);
-        const uint4 dv = *reinterpret_cast<const uint4*>(
-            reinterpret_cast<const __nv_bfloat16*>(a.dout) + orow + d0);
-        const uint32_t ou[4] = {ov.x, ov.y, ov.z, ov.w}, du[4] = {dv.x, dv.y, dv.z, dv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          o8[2 * e] = bf16_lo(ou[e]); o8[2 * e + 1] = bf16_hi(ou[e]);
-          do8[2 * e] = bf16_lo(du[e]); do8[2 * e + 1] = bf16_hi(du[e]);
-        }
-        if (a.g) {
-          const uint4 gv = *reinterpret_cast<const uint4*>(
-              reinterpret_cast<const __nv_bfloat16*>(a.g) + grow + d0);
-          const uint32_t gu[4] = {gv.x, gv.y, gv.z, gv.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) { g8[2 * e] = bf16_lo(gu[e]); g8[2 * e + 1] = bf16_hi(gu[e]); }
+        if (!F32) {
+          const float l = a.lse[(b * a.H + h) * a.Lq + q];
+          lv = sgn * (l == -INFINITY ? INFINITY : l * kLog2e);  // no kept key -> P = 0
         }
       }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) Dq = fmaf(do8[e], o8[e], Dq);
-      if (a.g) {
-        float da[8], dg[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float sg = F32 ? 1.f / (1.f + expf(-g8[e])) : 1.f / (1.f + __expf(-g8[e]));
-          da[e] = do8[e] * sg;
-          dg[e] = do8[e] * o8[e] * (1.f - sg);
-        }
-        if (F32) {
-          float* dap = reinterpret_cast<float*>(a.dA) + arow + d0;
-          float* dgp = reinterpret_cast<float*>(a.dg) + grow + d0;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) { dap[e] = da[e]; dgp[e] = dg[e]; }
-        } else {
-          uint4 x, y;
-          x.x = pack_bf16(da[0], da[1]); x.y = pack_bf16(da[2], da[3]);
-          x.z = pack_bf16(da[4], da[5]); x.w = pack_bf16(da[6], da[7]);
-          y.x = pack_bf16(dg[0], dg[1]); y.y = pack_bf16(dg[2], dg[3]);
-          y.z = pack_bf16(dg[4], dg[5]); y.w = pack_bf16(dg[6], dg[7]);
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow + d0) = x;
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dg) + grow + d0) = y;
-        }
-      }
+      sD[hi][qi] = sgn * Dq;
+      sL[hi][qi] = lv;
     }
-    a.Dvec[r] = sgn * Dq;
-    if (!F32) {
-      const float l = a.lse[bh * a.Lq + q];
-      a.lse2[r] = sgn * (l == -INFINITY ? INFINITY : l * kLog2e);  // no kept key -> P = 0
+    __syncthreads();
+    for (int r = threadIdx.x; r < 32 * hc; r += blockDim.x) {  // coalesced along q
+      const int hi = r / 32, qi = r % 32;
+      const int64_t v = (b * a.H + h0 + hi) * Lq_pad + q0 + qi;
+      a.Dvec[v] = sD[hi][qi];
+      if (!F32) a.lse2[v] = sL[hi][qi];
     }
+    __syncthreads();
   }
 }
 
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
-  const int64_t nrows = (int64_t)a.B * a.H * Lq_pad;
-  if (nrows == 0) return cudaSuccess;
-  const int64_t blocks = (nrows + 255) / 256;
-  const unsigned grid = (unsigned)(blocks < 148 * 32 ? blocks : 148 * 32);
-  if (f32) bwd_pre_kernel<true><<<grid, 256, 0, st>>>(a);
-  else bwd_pre_kernel<false><<<grid, 256, 0, st>>>(a);
+  const int64_t blocks = (int64_t)a.B * (Lq_pad / 32);
+  if (blocks == 0) return cudaSuccess;
+  if (f32) bwd_pre_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else bwd_pre_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -602,49 +614,81 @@ cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, 
 }
 
 // =============================================================================== reduce / convert
-// dbias[(b,) h, q, k] = Σ_c partial[c][(b,) h][q][k]   (partials padded to [.][Lq_pad][Lk_pad])
+// dbias[(b,) h, q, k] = Σ_c partial[c][(b,) h][q][k]   (partials padded to [.][Lq_pad][Lk_pad]).
+// Tiles of 32 q x 32 k: the partials are read along k (coalesced, 4 parts in flight) and the sum
+// is written along whichever of q/k is unit-stride in the destination (smem transpose for q).
 __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
+  __shared__ float tile[32][33];
   const int Lq_pad = ((a.Lq + 127) / 128) * 128, Lk_pad = ((a.Lk + 127) / 128) * 128;
-  const int64_t n = a.nb * a.H * (int64_t)a.Lq * a.Lk;
   const int64_t plane = (int64_t)a.H * Lq_pad * Lk_pad;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = idx;
-    int q, k;
-    if (a.q_fast) { q = (int)(t % a.Lq); t /= a.Lq; k = (int)(t % a.Lk); t /= a.Lk; }
-    else { k = (int)(t % a.Lk); t /= a.Lk; q = (int)(t % a.Lq); t /= a.Lq; }
-    const int h = (int)(t % a.H);
-    const int64_t bb = t / a.H;
-    const int64_t src = ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k;
-    float s = 0.f;
-    for (int c = 0; c < a.nparts; ++c) s += a.partial[c * plane + src];
-    a.dbias[bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + (int64_t)k * a.s_k] = s;
+  const int nqt = (a.Lq + 31) / 32, nkt = (a.Lk + 31) / 32;
+  int64_t u = blockIdx.x;
+  const int kt = (int)(u % nkt); u /= nkt;
+  const int qt = (int)(u % nqt); u /= nqt;
+  const int h = (int)(u % a.H);
+  const int64_t bb = u / a.H;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int k = kt * 32 + tx;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int qi = ty + 8 * i, q = qt * 32 + qi;
+    const float* src = a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int c = 0;
+    for (; c + 4 <= a.nparts; c += 4) {
+      s0 += src[(c + 0) * plane];
+      s1 += src[(c + 1) * plane];
+      s2 += src[(c + 2) * plane];
+      s3 += src[(c + 3) * plane];
+    }
+    for (; c < a.nparts; ++c) s0 += src[c * plane];
+    tile[qi][tx] = (s0 + s1) + (s2 + s3);
+  }
+  __syncthreads();
+  if (a.q_fast) {  // destination q-contiguous: lanes along q
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int ki = ty + 8 * i, q = qt * 32 + tx, kk = kt * 32 + ki;
+      if (q < a.Lq && kk < a.Lk)
+        a.dbias[bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + (int64_t)kk * a.s_k] = tile[tx][ki];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int qi = ty + 8 * i, q = qt * 32 + qi;
+      if (q < a.Lq && k < a.Lk)
+        a.dbias[bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + (int64_t)k * a.s_k] = tile[qi][tx];
+    }
   }
 }
 
 cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st) {
-  const int64_t n = a.nb * a.H * (int64_t)a.Lq * a.Lk;
-  if (n == 0) return cudaSuccess;
-  const int64_t blocks = (n + 255) / 256;
-  dbias_reduce_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(a);
+  const int64_t blocks = a.nb * a.H * (int64_t)((a.Lq + 31) / 32) * ((a.Lk + 31) / 32);
+  if (blocks == 0) return cudaSuccess;
+  dbias_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
+// dq = bf16(scale · Σ_p part_p): 8 elements per thread, rows visited in the order of the smaller
+// of the (h, l) strides of dq (the parts use the same order, see ws_layout)
 __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
-  const int64_t n8 = (int64_t)a.B * a.H * a.Lq * (a.D / 8);
+  const int nd = a.D / 8;
+  const int64_t n8 = (int64_t)a.B * a.H * a.Lq * nd;
+  const bool hfast = a.q_sh < a.q_sl;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n8;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int d0 = (int)(idx % (a.D / 8)) * 8;
-    const int64_t r = idx / (a.D / 8);
-    const int q = (int)(r % a.Lq);
-    const int64_t bh = r / a.Lq;
-    const int h = (int)(bh % a.H);
-    const int64_t b = bh / a.H;
-    float4 x = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0);
-    float4 y = *reinterpret_cast<const float4*>(a.acc + r * a.D + d0 + 4);
+    const int d0 = (int)(idx % nd) * 8;
+    int64_t r = idx / nd;
+    int h, q;
+    if (hfast) { h = (int)(r % a.H); r /= a.H; q = (int)(r % a.Lq); r /= a.Lq; }
+    else { q = (int)(r % a.Lq); r /= a.Lq; h = (int)(r % a.H); r /= a.H; }
+    const int64_t b = r;
+    const int64_t src = b * a.p_sb + h * a.p_sh + (int64_t)q * a.p_sl + d0;
+    float4 x = *reinterpret_cast<const float4*>(a.acc + src);
+    float4 y = *reinterpret_cast<const float4*>(a.acc + src + 4);
     for (int p = 1; p < a.nparts; ++p) {
-      const float4 x2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + r * a.D + d0);
-      const float4 y2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + r * a.D + d0 + 4);
+      const float4 x2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + src);
+      const float4 y2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + src + 4);
       x.x += x2.x; x.y += x2.y; x.z += x2.z; x.w += x2.w;
       y.x += y2.x; y.y += y2.y; y.z += y2.z; y.w += y2.w;
     }

@@ -245,25 +245,45 @@ __global__ void __launch_bounds__(352, 1)
       // biasᵀ[k][q] = bias[h, q, k0 + k] for q < Lq, k0 + k < Lk; 0 elsewhere (padding must be
       // finite: it meets zero P/dA rows in the MMAs)
       const __nv_bfloat16* bp = a.bias + (int64_t)h * a.b_sh;
-      if (a.b_sk == 1) {  // k-contiguous rows: lanes along k, 4 keys each
-        for (int q = tid >> 5; q < Lq_pad; q += 8) {
-          const int kl = lane * 4;
-          uint16_t v4[4] = {0, 0, 0, 0};
-          if (q < a.Lq) {
-            const __nv_bfloat16* src = bp + (int64_t)q * a.b_sq + k0 + kl;
-            if (k0 + kl + 3 < a.Lk) {
-              const uint2 u = *reinterpret_cast<const uint2*>(src);
-              v4[0] = u.x & 0xffff; v4[1] = u.x >> 16; v4[2] = u.y & 0xffff; v4[3] = u.y >> 16;
-            } else {
-              for (int e = 0; e < 4; ++e)
-                if (k0 + kl + e < a.Lk) v4[e] = __bfloat16_as_ushort(src[e]);
+      if (a.b_sk == 1) {
+        // k-contiguous rows: a lane loads 8 keys of one query (16 B) and scatters them down the
+        // 8 key rows of its column; the 32 lanes of a warp take 32 consecutive queries, so each
+        // 2-byte store instruction hits 4 swizzled chunks x 8 lanes = no bank conflict
+        const int nunits = (Lq_pad / 32) * 16;  // (32-query block, 8-key group) units
+        for (int u0 = w; u0 < nunits; u0 += 8 * 4) {
+          uint4 v[4];
+          int qq[4], kk8[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {  // 4 independent loads in flight per lane
+            const int u = u0 + x * 8;
+            qq[x] = (u / 16) * 32 + lane;
+            kk8[x] = (u % 16) * 8;
+            v[x] = make_uint4(0, 0, 0, 0);
+            if (u < nunits && qq[x] < a.Lq) {
+              const __nv_bfloat16* src = bp + (int64_t)qq[x] * a.b_sq + k0 + kk8[x];
+              if (k0 + kk8[x] + 7 < a.Lk) {
+                v[x] = *reinterpret_cast<const uint4*>(src);
+              } else {
+                uint16_t e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int e = 0; e < 8; ++e)
+                  if (k0 + kk8[x] + e < a.Lk) e8[e] = __bfloat16_as_ushort(src[e]);
+                v[x] = make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16),
+                                  e8[4] | (e8[5] << 16), e8[6] | (e8[7] << 16));
+              }
             }
           }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t r = kl + e;
-            const uint32_t addr = sBias + r * RB + ((((uint32_t)q >> 3) ^ (r & 7)) << 4) + (q & 7) * 2;
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v4[e]) : "memory");
+          for (int x = 0; x < 4; ++x) {
+            if (u0 + x * 8 >= nunits) break;
+            const uint32_t q = (uint32_t)qq[x];
+            const uint32_t w4[4] = {v[x].x, v[x].y, v[x].z, v[x].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const uint32_t r = (uint32_t)kk8[x] + e;
+              const uint16_t val = (uint16_t)(e & 1 ? w4[e >> 1] >> 16 : w4[e >> 1] & 0xffff);
+              const uint32_t addr = sBias + r * RB + (((q >> 3) ^ (r & 7)) << 4) + (q & 7) * 2;
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(val) : "memory");
+            }
           }
         }
       } else {  // q-contiguous rows: thread per key row, 8 queries per 16-B load

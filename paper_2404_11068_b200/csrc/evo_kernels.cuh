@@ -55,7 +55,8 @@ struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
   const float* lse;
   float* lse2;   // lse*log2e, +inf for rows with no kept key (bf16 path) | lse (f32 path)
   float* Dvec;   // Σ_d dO·o
-  void* dA;      // [B,H,Lq,D] contiguous dO·sigmoid(g) (NULL when no gate)
+  void* dA;      // dO·sigmoid(g) (NULL when no gate), element strides below, d unit-stride
+  int64_t a_sb, a_sh, a_sl;
   int negate;    // store -lse2 and -D (the fused backward's operand form)
 };
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st);
@@ -166,6 +167,7 @@ struct ConvertArgs {  // dq = bf16(scale * Σ_p acc[p])
   const float* acc;
   int nparts;
   int64_t part_stride;  // elements between parts
+  int64_t p_sb, p_sh, p_sl;  // element strides of one part (d unit-stride)
   __nv_bfloat16* dq;
   int64_t q_sb, q_sh, q_sl;
 };
