@@ -65,6 +65,8 @@ def kernel_alg(name, B, H, L, D, bias):
         return 8.0 * P * D, 14.0 * X + 8.0 * B * H * L + bb + B * L, float(P)
     if name == "bwd_bias":  # dbias (fp32) written once; inputs already counted in bwd_main
         return 0.0, 2.0 * bb, float(P)
+    if name == "bwd_fused":  # q,k,v,dA + lse2/D + bias + mask in; dq,dk,dv (bf16) + dbias out
+        return 8.0 * P * D, 14.0 * X + 8.0 * B * H * L + 3.0 * bb + B * L, float(P)
     if name in ("dq_convert",):
         return 0.0, 6.0 * X, 0.0
     if name == "dbias_reduce":
@@ -313,11 +315,11 @@ def run_gpu(args):
     calls = []
     for name, B, H, L, bias in MODULES:
         calls.append(("fwd_bf16", B, H, L, bias))
-        calls += [("bwd_pre", B, H, L, bias), ("bwd_main", B, H, L, bias)]
+        calls += [("bwd_pre", B, H, L, bias), ("bwd_fused", B, H, L, bias)]
         if L > 128:
             calls.append(("dq_convert", B, H, L, bias))
         if bias:
-            calls += [("bwd_bias", B, H, L, bias), ("dbias_reduce", B, H, L, bias)]
+            calls.append(("dbias_reduce", B, H, L, bias))
     work = {}
     for kname, B, H, L, bias in calls:
         f, by, ex = kernel_alg(kname, B, H, L, C_HEAD, bias)
@@ -388,7 +390,8 @@ def load_traffic(kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get(kernel)
+            v = json.load(open(p)).get(kernel)
+            return float(v) if isinstance(v, (int, float)) else None
         except Exception:
             return None
     return None
