@@ -8,7 +8,7 @@
 // hand-scheduled warp-specialised pipeline whose cross-warp hand-offs sit on the critical path.
 //
 // Per CTA (thread = query row = TMEM lane; thread 0 also issues TMA and tcgen05.mma):
-//   TMEM (128 cols for D <= 32):  S|P [0,64)  O [64, 64+DP)  Q [96, 96+DP/2)
+//   TMEM (128 cols for D <= 32):  S|P [0,64)  O [64, 64+DP)  Q [96, 96+DP/2)  G [.., +DP/2)
 //   Q row -> TMEM once (tcgen05.st), then per 64-key chunk c (K/V/bias double-buffered by TMA):
 //     S  = Q·K_cᵀ            tcgen05.mma, A = Q from TMEM (TS form), N = 64
 //     x  = S·scale + bias    f32x2 FMA; hard mask; chunk max (3-input max)
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128, 4)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(w * 32) << 16;
-  const uint32_t tS = tmem + C::cS, tO = tmem + C::cO, tQ = tmem + C::cQ;
+  const uint32_t tS = tmem + C::cS, tO = tmem + C::cO, tQ = tmem + C::cQ, tG = tQ + DP / 2;
   const int bc = a.bias_batched ? b : 0;
   auto load_chunk = [&](int c) {  // thread 0 only
     const int st = c & 1;
@@ -99,19 +99,16 @@ __global__ void __launch_bounds__(128, 4)
     umma_commit(bar_s);
   };
   // The first K/V/bias chunks (TMA), this thread's Q row and its gate row are all in flight
-  // together; Q then goes straight into this thread's TMEM lane, the gate row stays in registers
-  // for the epilogue (its latency is otherwise exposed at the end of every unit).
-  unsigned long long* dbg = (a.dbg && blockIdx.x < 148) ? a.dbg + (size_t)blockIdx.x * 512 : nullptr;
+  // together (the gate's latency is otherwise exposed at the end of every unit).
   if (tid == 0) {
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     if (BIAS) tma_prefetch_desc(&tm_b);
-    if (dbg) { dbg[0] = clock64(); dbg[1] = clock64(); }
     load_chunk(0);
     if (nc > 1) load_chunk(1);
   }
-  uint32_t qrow[DP / 2], gpk[DP / 2];
   {
+    uint32_t qrow[DP / 2], gpk[DP / 2];
     const __nv_bfloat16* qp = qptr + (int64_t)b * q_sb + (int64_t)h * q_sh + (int64_t)q * q_sl;
     const __nv_bfloat16* gp = a.g + (int64_t)b * a.g_sb + (int64_t)h * a.g_sh + (int64_t)q * a.g_sl;
 #pragma unroll
@@ -124,17 +121,25 @@ __global__ void __launch_bounds__(128, 4)
       qrow[d0 / 2] = v.x; qrow[d0 / 2 + 1] = v.y; qrow[d0 / 2 + 2] = v.z; qrow[d0 / 2 + 3] = v.w;
       gpk[d0 / 2] = gv.x; gpk[d0 / 2 + 1] = gv.y; gpk[d0 / 2 + 2] = gv.z; gpk[d0 / 2 + 3] = gv.w;
     }
+  // Q row and the gate row (packed bf16) go to this thread's TMEM lane: Q is the A operand of
+  // Sᵀ's TS-form MMA, the gate waits there for the epilogue (no registers held across the loop)
+  if (DP == 16) {
+    tmem_st8(tQ + lane_base, *reinterpret_cast<uint32_t(*)[8]>(qrow));
+    tmem_st8(tG + lane_base, *reinterpret_cast<uint32_t(*)[8]>(gpk));
+  } else if (DP == 32) {
+    tmem_st16(tQ + lane_base, *reinterpret_cast<uint32_t(*)[16]>(qrow));
+    tmem_st16(tG + lane_base, *reinterpret_cast<uint32_t(*)[16]>(gpk));
+  } else {
+    tmem_st32(tQ + lane_base, *reinterpret_cast<uint32_t(*)[32]>(qrow));
+    tmem_st32(tG + lane_base, *reinterpret_cast<uint32_t(*)[32]>(gpk));
   }
-  if (DP == 16) tmem_st8(tQ + lane_base, *reinterpret_cast<uint32_t(*)[8]>(qrow));
-  else if (DP == 32) tmem_st16(tQ + lane_base, *reinterpret_cast<uint32_t(*)[16]>(qrow));
-  else tmem_st32(tQ + lane_base, *reinterpret_cast<uint32_t(*)[32]>(qrow));
+  }
   tmem_wait_st();
   tc_fence_before();
   __syncthreads();  // Q in TMEM
   if (tid == 0) {
     tc_fence_after();
     mbar_wait(bar_kv0, 0);
-    if (dbg) dbg[2] = clock64();
     issue_S(0);
   }
 
@@ -161,9 +166,7 @@ __global__ void __launch_bounds__(128, 4)
       mw0 = __ballot_sync(0xffffffffu, r0 != 0);
       mw1 = __ballot_sync(0xffffffffu, r1 != 0);
     }
-    if (dbg && tid == 0 && c < 8) dbg[256 + c * 4 + 0] = clock64();
     mbar_wait(bar_s, c & 1);
-    if (dbg && tid == 0 && c < 8) dbg[256 + c * 4 + 1] = clock64();
     tc_fence_after();
     float x[64];
     {
@@ -261,9 +264,7 @@ __global__ void __launch_bounds__(128, 4)
     tmem_st32(tS + lane_base, pk);  // P over the consumed S columns [0, 32)
     tmem_wait_st();
     tc_fence_before();
-    if (dbg && tid == 0 && c < 8) dbg[256 + c * 4 + 2] = clock64();
     __syncthreads();  // all P written; S_c fully consumed; bias stage read
-    if (dbg && tid == 0 && c < 8) dbg[256 + c * 4 + 3] = clock64();
     if (tid == 0) {
       tc_fence_after();
       const uint32_t vb = sb + C::kKV;
@@ -275,18 +276,14 @@ __global__ void __launch_bounds__(128, 4)
       if (c + 1 < nc) {
         // S_{c+1} overwrites the P columns: wait for PV_c, which also frees stage `st`
         mbar_wait(bar_o, c & 1);
-        if (dbg && c + 2 < 8) dbg[(c + 2) * 4 + 1] = clock64();
         if (c + 2 < nc) load_chunk(c + 2);
-        if (dbg && c + 1 < 8) dbg[(c + 1) * 4 + 0] = clock64();
         mbar_wait(bar_kv0 + 8 * ((c + 1) & 1), ((c + 1) >> 1) & 1);
-        if (dbg && c + 1 < 8) dbg[(c + 1) * 4 + 2] = clock64();
         issue_S(c + 1);
       }
     }
   }
   // ---- epilogue
   mbar_wait(bar_o, (nc - 1) & 1);
-  if (dbg && tid == 0) dbg[299] = clock64();
   tc_fence_after();
   uint32_t ov[DP];
   if (DP == 16) {
@@ -305,6 +302,11 @@ __global__ void __launch_bounds__(128, 4)
       for (int i = 0; i < 32; ++i) ov[c0 + i] = r[i];
     }
   }
+  uint32_t gpk[DP / 2];
+  if (DP == 16) tmem_ld8(tG + lane_base, *reinterpret_cast<uint32_t(*)[8]>(gpk));
+  else if (DP == 32) tmem_ld16(tG + lane_base, *reinterpret_cast<uint32_t(*)[16]>(gpk));
+  else tmem_ld32(tG + lane_base, *reinterpret_cast<uint32_t(*)[32]>(gpk));
+  tmem_wait_ld();
   if (qv) {
     const float inv = l_run > 0.f ? fast_rcp(l_run) : 0.f;
     __nv_bfloat16* op = a.o + (int64_t)b * a.o_sb + (int64_t)h * a.o_sh + (int64_t)q * a.o_sl;
@@ -333,7 +335,6 @@ __global__ void __launch_bounds__(128, 4)
     a.lse[((int64_t)b * a.H + h) * a.Lq + q] =
         l_run > 0.f ? (m_ref == -INFINITY ? 0.f : m_ref) + __logf(l_run) : -INFINITY;
   }
-  if (dbg && tid == 0) dbg[300] = clock64();
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<C::kTmemCols>(tmem);
