@@ -276,33 +276,60 @@ def run_gpu(args):
         step()
     torch.cuda.synchronize()
 
+    # CUDA graph of the whole step (graphs remove the per-launch host overhead);
+    # the C-ABI calls are stream-ordered and allocation-free, so they capture as they are
+    graph = None
+    launches_per_step = 0
+    if not args.no_graph:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            step()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                launches_per_step = step()
+        torch.cuda.synchronize()
+
     # timed region: K steps, L2 flushed (256 MB write) before each, CUDA events per step
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    launches = 0
+    for s in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        ev[s][0].record(stream)
+        if graph is not None:
+            graph.replay()
+            launches += launches_per_step
+        else:
+            launches += step()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    clk = clocks.stop()
+
+    # per-kernel device time: the same K steps again, eager, each launch bracketed by CUDA
+    # events on its stream (events cannot be timed inside a graph replay)
     nk_per_step = 64
     trace_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nk_per_step * args.steps)]
     for e in trace_ev:  # torch creates events lazily: materialise the handles first
         e.record(stream)
     torch.cuda.synchronize()
     trace_arr = (__import__("ctypes").c_void_p * len(trace_ev))(*[e.cuda_event for e in trace_ev])
-    clocks = ClockSampler(0)
-    clocks.start()
-    time.sleep(0.3)
-    torch.cuda.synchronize()
     lib.evo_trace_enable(trace_arr, len(trace_ev))
-    launches = 0
     for s in range(args.steps):
         if not args.no_flush:
             flush.zero_()
-        ev[s][0].record(stream)
-        launches += step()
-        ev[s][1].record(stream)
+        step()
     torch.cuda.synchronize()
     ntr = lib.evo_trace_count()
     labels = [lib.evo_trace_label(i).decode() for i in range(ntr)]
     lib.evo_trace_enable(None, 0)
-    clk = clocks.stop()
-    ms = [a.elapsed_time(b) for a, b in ev]
     ms_step = float(np.mean(ms))
     flops = sum(alg_flops(B, H, L, C_HEAD) for _, B, H, L, _ in MODULES)
     value = flops / (ms_step * 1e-3) / 1e12
@@ -372,7 +399,9 @@ def run_gpu(args):
                    "modules": {m[0]: {"B": m[1], "H": m[2], "L": m[3], "D": C_HEAD,
                                       "bias": m[4]} for m in MODULES},
                    "l2": "flushed (256 MB write) before every timed step" if not args.no_flush
-                   else "warm", "parallelism": "single GPU"},
+                   else "warm", "parallelism": "single GPU",
+                   "launch": "CUDA graph of the step" if graph is not None else "eager",
+                   "kernel_timing": "per-launch CUDA events over K further eager steps"},
         "pct_of_peak": {"tensor_measured": value / pk["bf16_tflops"],
                         "tensor_nominal": value / 2250.0},
         "roofline": roof,
@@ -470,6 +499,7 @@ def main():
     ap.add_argument("--impl", choices=["evo", "reference"], default="evo")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=2,
                     help="--impl reference: batch rows of each module per step")

@@ -18,7 +18,7 @@ namespace evo {
 // CTA per (b, 32 query rows) x all heads.  Rows are visited in the order of the smaller of the
 // (h, l) strides of o, so a warp's 16-byte loads/stores cover consecutive memory; the per-row
 // statistics go through shared memory and leave as coalesced [B*H][Lq_pad] vectors.
-template <bool F32>
+template <bool F32, int DP>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
   constexpr int kHC = 16;  // heads per pass
   __shared__ float sD[kHC][32], sL[kHC][32];
@@ -38,7 +38,9 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
         const int64_t orow = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl;
         const int64_t grow = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl;
         const int64_t arow = b * a.a_sb + h * a.a_sh + (int64_t)q * a.a_sl;
-        for (int d0 = 0; d0 < a.D; d0 += 8) {
+#pragma unroll
+        for (int d0 = 0; d0 < DP; d0 += 8) {  // unrolled: every row load in flight at once
+          if (d0 >= a.D) break;
           float o8[8], do8[8], g8[8];
           if (F32) {
             const float* op = reinterpret_cast<const float*>(a.o) + orow + d0;
@@ -118,8 +120,16 @@ cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
   const int64_t blocks = (int64_t)a.B * (Lq_pad / 32);
   if (blocks == 0) return cudaSuccess;
-  if (f32) bwd_pre_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(a);
-  else bwd_pre_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(a);
+  const unsigned g = (unsigned)blocks;
+  if (f32) {
+    if (a.D <= 16) bwd_pre_kernel<true, 16><<<g, 256, 0, st>>>(a);
+    else if (a.D <= 32) bwd_pre_kernel<true, 32><<<g, 256, 0, st>>>(a);
+    else bwd_pre_kernel<true, 64><<<g, 256, 0, st>>>(a);
+  } else {
+    if (a.D <= 16) bwd_pre_kernel<false, 16><<<g, 256, 0, st>>>(a);
+    else if (a.D <= 32) bwd_pre_kernel<false, 32><<<g, 256, 0, st>>>(a);
+    else bwd_pre_kernel<false, 64><<<g, 256, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -633,16 +643,15 @@ __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
   for (int i = 0; i < 4; ++i) {
     const int qi = ty + 8 * i, q = qt * 32 + qi;
     const float* src = a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int c = 0;
-    for (; c + 4 <= a.nparts; c += 4) {
-      s0 += src[(c + 0) * plane];
-      s1 += src[(c + 1) * plane];
-      s2 += src[(c + 2) * plane];
-      s3 += src[(c + 3) * plane];
+    float acc = 0.f;
+    for (int c0 = 0; c0 < a.nparts; c0 += 16) {  // up to 16 independent loads in flight
+      float v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = c0 + c < a.nparts ? src[(int64_t)(c0 + c) * plane] : 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc += v[c];  // fixed order: deterministic
     }
-    for (; c < a.nparts; ++c) s0 += src[c * plane];
-    tile[qi][tx] = (s0 + s1) + (s2 + s3);
+    tile[qi][tx] = acc;
   }
   __syncthreads();
   if (a.q_fast) {  // destination q-contiguous: lanes along q
