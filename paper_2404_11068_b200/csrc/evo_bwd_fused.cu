@@ -25,6 +25,9 @@
 // TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | 2 x (Sᵀ 32 | dPᵀ 32) | dV DP | dK DP | dQ DP
 // SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 |
 //       Q,dA x2 | Pᵀ x2 (8 KB) | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
+#include <cstdio>
+#include <cstdlib>
+
 #include "evo_kernels.cuh"
 
 namespace evo {
@@ -43,7 +46,8 @@ struct FusedCfg {
   static constexpr uint32_t oStK = oVec + 2048;          // staging: dK, dV bf16, dQ bf16|fp32
   static constexpr uint32_t oStV = oStK + kTile;
   static constexpr uint32_t oStQ = oStV + kTile;
-  static constexpr uint32_t oBar = oStQ + 128 * DP * 4;
+  static constexpr uint32_t oRecv = oStQ + 128 * DP * 4;  // peer's dQ rows (64 x DP fp32)
+  static constexpr uint32_t oBar = oRecv + 64 * DP * 4;
   static constexpr uint32_t kSmem = oBar + 256;
 };
 
@@ -76,13 +80,17 @@ __global__ void __launch_bounds__(352, 1)
   const uint32_t bar_dq = smem_u32(&bars[14]);      // dQ MMA of a query tile (and all before) done
   const uint32_t bar_dkvfree = smem_u32(&bars[15]); // group 0 pulled a finished dK/dV (4 warps)
   const uint32_t bar_mm = smem_u32(&bars[16]);      // +8: group 1   dV/dK of its sub-tile done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[18]);
+  const uint32_t bar_xfull = smem_u32(&bars[18]);   // pair: the peer's dQ rows landed (2 warps)
+  const uint32_t bar_xfree = smem_u32(&bars[19]);   // pair: the peer consumed ours (2 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[20]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
   const int Lq_pad = nq * 128, Lk_pad = nk * 128;
-  const int c = blockIdx.x % a.nchunks;
-  const int grp = blockIdx.x / a.nchunks;
+  // pair mode: a cluster of 2 = the two key tiles of one (h, chunk); else (h, kt, chunk) flat
+  const int pr = a.pairx ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int c = a.pairx ? pr % a.nchunks : (int)blockIdx.x % a.nchunks;
+  const int grp = a.pairx ? (pr / a.nchunks) * 2 + (int)(blockIdx.x & 1) : (int)blockIdx.x / a.nchunks;
   const int kt = grp % nk, h = grp / nk;
   const int k0 = kt * 128;
   const int b0 = c * a.chunk;
@@ -106,10 +114,15 @@ __global__ void __launch_bounds__(352, 1)
     }
     mbar_init(bar_dq, 1);
     mbar_init(bar_dkvfree, 4);
+    mbar_init(bar_xfull, 2);
+    mbar_init(bar_xfree, 2);
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
+  // pair mode: both CTAs of the cluster start their identical schedules together, so the dQ
+  // halves they exchange one sub-tile apart arrive before they are needed
+  if (a.pairx) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t cb = BIAS ? (uint32_t)Lq_pad : 0u;
@@ -335,9 +348,23 @@ __global__ void __launch_bounds__(352, 1)
     // bar_dq wait (all MMAs up to that tile's dQ complete).  dK/dV are pulled first and released
     // on bar_dkvfree (the next batch row's first dV/dK MMA overwrites them); the dQ part stays
     // valid until the next tile's dQ MMA, which waits for this group's next hand-off.
-    auto drain = [&](int bq, int q0, bool kv, int bk, bool release_kv) {
-      if (tid == 0) bulk_wait_group_read0();  // the previous drain's stores left the staging
-      named_bar_sync(2, 128);
+    // the thread that issues (and waits for) this CTA's TMA stores: in pair mode a thread of the
+    // 64-row half this CTA finalises
+    const int io_tid = a.pairx ? kt * 64 : 0;
+    // Drains (group 0).  dK/dV of batch row bk (kv); the dQ part of (bq, query tile at q0):
+    //  - single key tile: bf16 rows of the tile (dqmode 0)
+    //  - > 2 key tiles: this key tile's fp32 part (dqmode 0; dq_convert sums them)
+    //  - pair mode (2 key tiles, cluster of 2): CTA kt finalises rows [64·kt, 64·kt+64); at the
+    //    first sub-tile after the tile it SENDS the other half of its part to the peer over DSMEM
+    //    (dqmode 1), and one sub-tile later (dQ still in TMEM: the next dQ MMA waits for this
+    //    group's next hand-off) it ADDS the peer's half to its own and stores bf16 (dqmode 2), so
+    //    the peer's data has had a whole sub-tile to arrive.
+    auto drain = [&](int bq, int q0, bool kv, int bk, bool release_kv, int dqmode, int xt) {
+      const bool store_q = dqmode != 1;
+      if (kv || store_q) {
+        if (tid == io_tid) bulk_wait_group_read0();  // earlier stores left the staging tiles
+        named_bar_sync(2, 128);
+      }
       uint32_t r[DP];
       if (kv) {
         tmem_ld_cols(tdK + lane_base, r);
@@ -352,19 +379,65 @@ __global__ void __launch_bounds__(352, 1)
         }
         stage_bf16(s0 + C::oStV, r, 1.f);
       }
-      tmem_ld_cols(tdQ + lane_base, r);
-      tmem_wait_ld();
-      if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
-      else stage_f32(s0 + C::oStQ, r);
-      fence_proxy_async_smem();
-      named_bar_sync(2, 128);
-      if (tid == 0) {
-        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
-        if (kv) {
-          tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
-          tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
+      constexpr uint32_t kRx = DP * 4;  // receive row bytes (fp32)
+      const int xrow = row & 63;
+      const bool mine = (qd >> 1) == kt;  // this thread's query row is in the half CTA kt owns
+      if (dqmode == 1) {
+        if (!mine) {
+          tmem_ld_cols(tdQ + lane_base, r);
+          tmem_wait_ld();
+          if (xt > 0) mbar_wait_cluster(bar_xfree, (xt - 1) & 1);
+          const uint32_t dst = mapa_shared(s0 + C::oRecv, (uint32_t)(kt ^ 1));
+#pragma unroll
+          for (int i = 0; i < DP / 4; ++i)
+            st_cluster_v4(dst + swz_offset(xrow, i, kRx), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                          r[4 * i + 3]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(mapa_shared(bar_xfull, (uint32_t)(kt ^ 1)));
         }
-        bulk_commit_group();
+      } else if (dqmode == 2) {
+        if (mine) {
+          tmem_ld_cols(tdQ + lane_base, r);
+          tmem_wait_ld();
+          mbar_wait_cluster(bar_xfull, xt & 1);
+#pragma unroll
+          for (int i = 0; i < DP / 4; ++i) {
+            const uint4 v = ld_shared_v4(s0 + C::oRecv + swz_offset(xrow, i, kRx));
+            r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + __uint_as_float(v.x));
+            r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + __uint_as_float(v.y));
+            r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + __uint_as_float(v.z));
+            r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + __uint_as_float(v.w));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(mapa_shared(bar_xfree, (uint32_t)(kt ^ 1)));
+#pragma unroll
+          for (int i = 0; i < DP / 8; ++i)
+            st_shared_v4(s0 + C::oStQ + swz_offset(xrow, i, kRbB),
+                         pack_bf16(__uint_as_float(r[8 * i]) * a.scale, __uint_as_float(r[8 * i + 1]) * a.scale),
+                         pack_bf16(__uint_as_float(r[8 * i + 2]) * a.scale, __uint_as_float(r[8 * i + 3]) * a.scale),
+                         pack_bf16(__uint_as_float(r[8 * i + 4]) * a.scale, __uint_as_float(r[8 * i + 5]) * a.scale),
+                         pack_bf16(__uint_as_float(r[8 * i + 6]) * a.scale, __uint_as_float(r[8 * i + 7]) * a.scale));
+        }
+      } else {
+        tmem_ld_cols(tdQ + lane_base, r);
+        tmem_wait_ld();
+        if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
+        else stage_f32(s0 + C::oStQ, r);
+      }
+      if (kv || store_q) {
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (tid == io_tid) {
+          if (store_q) {
+            if (dqmode == 2) tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0 + 64 * kt, h, bq);
+            else tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
+          }
+          if (kv) {
+            tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
+            tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
+          }
+          bulk_commit_group();
+        }
       }
     };
     // hard-mask bit of this thread's key for batch row b (prefetched one batch row ahead)
@@ -479,7 +552,10 @@ __global__ void __launch_bounds__(352, 1)
       if (rec) DBG(j * 8 + 5);
       if (drain_now) {  // group 0: the previous query tile's dQ part (+ dK/dV at a new row)
         const int Tp = T - 1;
-        drain(b0 + Tp / nq, (Tp % nq) * 128, t == 0, b - 1, true);
+        drain(b0 + Tp / nq, (Tp % nq) * 128, t == 0, b - 1, true, a.pairx ? 1 : 0, Tp);
+      } else if (a.pairx && g == 0 && s == 2 && T > 0) {  // pair: finish the previous tile's dQ
+        const int Tp = T - 1;
+        drain(b0 + Tp / nq, (Tp % nq) * 128, false, 0, false, 2, Tp);
       }
       s += 2;
       if (s >= 4) {
@@ -492,8 +568,13 @@ __global__ void __launch_bounds__(352, 1)
       const int Tl = (J >> 2) - 1;
       mbar_wait(bar_dq, Tl & 1);
       tc_fence_after();
-      drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false);
-      if (tid == 0) bulk_wait_group0();
+      if (a.pairx) {
+        drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false, 1, Tl);
+        drain(b0 + Tl / nq, (Tl % nq) * 128, false, 0, false, 2, Tl);
+      } else {
+        drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false, 0, Tl);
+      }
+      if (tid == io_tid) bulk_wait_group0();
     }
     if (BIAS) {  // partial[c][h][q][k0 + row]: this group's 32-query column blocks
       float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
@@ -508,6 +589,7 @@ __global__ void __launch_bounds__(352, 1)
   }
 #undef DBG
   tc_fence_before();
+  if (a.pairx) cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
   __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
 }
@@ -521,9 +603,31 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
-  kern<<<(unsigned)grid, 352, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
-                                          L.tm_dv, L.args);
-  return cudaGetLastError();
+  if (!L.args.pairx) {
+    kern<<<(unsigned)grid, 352, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
+                                            L.tm_dv, L.args);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(352);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (getenv("EVO_DEBUG_CLUSTERS")) {
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+    fprintf(stderr, "bwd_fused pair mode: grid %lld CTAs = %lld clusters, max active %d\n", grid,
+            grid / 2, ncl);
+  }
+  return cudaLaunchKernelEx(&cfg, kern, L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk, L.tm_dv,
+                            L.args);
 }
 
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {

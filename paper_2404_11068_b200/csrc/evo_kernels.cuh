@@ -129,6 +129,7 @@ struct BwdFusedArgs {
   float* dq_acc;      // otherwise [nk][B,H,Lq,D] fp32: key tile kt's dQ part (plain stores)
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
   unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
+  int pairx;  // two key tiles: CTA pair (cluster of 2) sums dQ over DSMEM, bf16 dq via TMA
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da;

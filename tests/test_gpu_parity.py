@@ -103,3 +103,13 @@ def test_gradient_identities():
     assert float(db.sum(-1).abs().max()) <= 2e-2 * float(db.abs().max()) * 16
     dk = out["dk"].double()
     assert float(dk.sum(2).abs().max()) <= 2e-2 * float(dk.abs().max()) * 16
+
+
+@pytest.mark.parametrize("bias_t", [False, True])
+def test_bf16_parity_pair_mode(monkeypatch, bias_t):
+    """The opt-in cluster-pair dQ exchange of the fused backward (EVO_BWD_PAIRX=1, two key
+    tiles) against the oracle."""
+    monkeypatch.setenv("EVO_BWD_PAIRX", "1")
+    errs, _, _ = run_case(3, 2, 256, 256, 32, seed=5, bias="shared", bias_t=bias_t, gate=True,
+                          mask="prefix", mask_t=False, layout="blhd")
+    _assert(errs, torch.bfloat16, f"pair mode bias_t={bias_t}")
