@@ -7,9 +7,10 @@
 // 32-query sub-tiles, and accumulates Σ_b dSᵀ for its key tile in TMEM (fp32, read-modify-write
 // by the owning thread), so the separate dbias pass and its second recompute disappear.
 //
-// Roles (352 threads): two compute warpgroups (warps 0-3, 4-7) take alternate sub-tiles
-// (ping-pong: one group's exp/ALU work covers the other's hand-offs and drains); warp 8 lane 0
-// issues the Sᵀ/dPᵀ MMAs, warp 10 lane 0 the dV/dK/dQ MMAs, warp 9 lane 0 the TMA loads.  Thread = key row k = TMEM lane.
+// Roles (384 threads): two compute warpgroups (warps 0-3, 4-7) take alternate sub-tiles
+// (ping-pong: one group's exp/ALU work covers the other's hand-offs and drains); warps 8 and 11
+// (lane 0) issue the Sᵀ/dPᵀ MMAs of group 0 / group 1, warp 10 lane 0 the dV/dK/dQ MMAs, warp 9
+// lane 0 the TMA loads.  Thread = key row k = TMEM lane.
 // Per sub-tile j (queries q0..q0+31 of batch row b), group g = j & 1:
 //   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 32 queries) -> TMEM slot g
 //   compute:  Pᵀ = exp2(Sᵀ·scale·log2e + biasᵀ·log2e − lse2), dSᵀ = Pᵀ⊙(dPᵀ − D)
@@ -58,7 +59,7 @@ EVO_DEV void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
 }
 
 template <int DP, bool BIAS>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(384, 1)
     bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_da,
                      const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(352, 1)
         }
       }
     }
-  } else if (w == 8) {
-    // ------------------------------------------------------------------ MMA issuer
+  } else if (w == 8 || w == 11) {
+    // ------------------------------------------------------------------ Sᵀ/dPᵀ MMA issuers
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 32, 0, 0);   // Sᵀ, dPᵀ
       // Sᵀ/dPᵀ of sub-tile i+2 starts as soon as its group has pulled sub-tile i out of the TMEM
@@ -166,8 +167,6 @@ __global__ void __launch_bounds__(352, 1)
       // apart, so this fixed blocking order never waits on an event that a later step produces.
       auto issue_s = [&](int j, int bi, int t, int s) {
         const int T = bi * nq + t, st = T & 1, kvs = bi & 1, g = j & 1;
-        if (s == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
-        if (s == 0 && t == 0) mbar_wait(bar_kv + 8 * kvs, (bi >> 1) & 1);
         if (j < 256) DBG(2048 + j * 4 + 0);
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
@@ -190,11 +189,22 @@ __global__ void __launch_bounds__(352, 1)
           if (++t == nq) { t = 0; ++bi; }
         }
       };
-      int sbi = 0, stt = 0, sss = 0;
-      for (int j = 0; j < J; ++j) {
-        if (j >= 2) mbar_wait(bar_sfree + 8 * (j & 1), ((j - 2) >> 1) & 1);
+      // one Sᵀ issuer per compute group (warp 8: even sub-tiles, warp 11: odd ones), so neither
+      // group's next Sᵀ waits on the other group's progress
+      const int gi = w == 8 ? 0 : 1;
+      int sbi = 0, stt = 0, sss = gi;
+      for (int j = gi; j < J; j += 2) {
+        if (j >= 2) mbar_wait(bar_sfree + 8 * gi, ((j - 2) >> 1) & 1);
+        // the first Sᵀ of this group in a tile / batch row waits for its inputs
+        const int T = sbi * nq + stt;
+        if (sss == gi) mbar_wait(bar_in + 8 * (T & 1), (T >> 1) & 1);
+        if (sss == gi && stt == 0) mbar_wait(bar_kv + 8 * (sbi & 1), (sbi >> 1) & 1);
         issue_s(j, sbi, stt, sss);
-        advance(sbi, stt, sss);
+        sss += 2;
+        if (sss >= 4) {
+          sss -= 4;
+          if (++stt == nq) { stt = 0; ++sbi; }
+        }
       }
     }
   } else if (w == 10) {
@@ -604,13 +614,13 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
   if (!L.args.pairx) {
-    kern<<<(unsigned)grid, 352, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
+    kern<<<(unsigned)grid, 384, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
                                             L.tm_dv, L.args);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(352);
+  cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
