@@ -30,6 +30,8 @@ CASES = [
     (1, 1, 1, 16, "shared", False, True, "none", False, "bhld"),         # L = 1
     (2, 2, 17, 32, "shared", True, False, "prefix", False, "blhd"),      # tiny ragged, bias^T
     (2, 1, 384, 32, "shared", False, True, "prefix", False, "blhd"),     # cfg5-like L
+    (2, 2, 520, 8, None, False, True, "prefix", True, "lbhd"),           # extra-MSA-like, 5 tiles
+    (2, 1, 384, 32, None, False, True, "prefix_fm", False, "blhd"),      # no bias, 3 key tiles
 ]
 
 
