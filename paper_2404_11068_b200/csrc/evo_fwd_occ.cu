@@ -28,7 +28,10 @@ struct OccCfg {
   static constexpr uint32_t kKV = 64 * kRowBytes;            // one 64-key K (or V) chunk
   static constexpr uint32_t kBias = BIAS ? 16384u : 0u;      // 128 x 64 bf16
   static constexpr uint32_t kStage = 2 * kKV + kBias;
-  static constexpr uint32_t kSmem = 2 * kStage + 64;         // 2 stages + barriers
+  // K/V(/bias) ring depth: 2 stages with a bias tile (smem-bound at 4 CTAs/SM), 4 without (long
+  // key sequences otherwise expose the TMA latency)
+  static constexpr int kNSt = BIAS ? 2 : 4;
+  static constexpr uint32_t kSmem = kNSt * kStage + 128;     // stages + barriers
   static constexpr uint32_t kTmemCols = DP <= 32 ? 128 : 256;
   static constexpr uint32_t cS = 0, cO = 64, cQ = DP <= 32 ? 96 : 128;
 };
@@ -44,11 +47,11 @@ __global__ void __launch_bounds__(128, 4)
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s0 = smem_u32(smem);
   if (s0 & 1023u) __trap();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * C::kStage);
-  const uint32_t bar_kv0 = smem_u32(&bars[0]);  // +8: stage 1
-  const uint32_t bar_s = smem_u32(&bars[2]);
-  const uint32_t bar_o = smem_u32(&bars[3]);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[4]);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kNSt * C::kStage);
+  const uint32_t bar_kv0 = smem_u32(&bars[0]);  // +8·s: stage s
+  const uint32_t bar_s = smem_u32(&bars[C::kNSt]);
+  const uint32_t bar_o = smem_u32(&bars[C::kNSt + 1]);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[C::kNSt + 2]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7;
@@ -61,8 +64,7 @@ __global__ void __launch_bounds__(128, 4)
 
   if (w == 0) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
   if (tid == 32) {
-    mbar_init(bar_kv0, 1);
-    mbar_init(bar_kv0 + 8, 1);
+    for (int i = 0; i < C::kNSt; ++i) mbar_init(bar_kv0 + 8 * i, 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_o, 1);
     fence_barrier_init();
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(128, 4)
   const uint32_t tS = tmem + C::cS, tO = tmem + C::cO, tQ = tmem + C::cQ, tG = tQ + DP / 2;
   const int bc = a.bias_batched ? b : 0;
   auto load_chunk = [&](int c) {  // thread 0 only
-    const int st = c & 1;
+    const int st = c % C::kNSt;
     const uint32_t sb = s0 + st * C::kStage;
     const uint32_t bar = bar_kv0 + 8 * st;
     mbar_arrive_expect_tx(bar, C::kStage);
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(128, 4)
   constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, 0, 0);
   constexpr uint32_t idesc_o = make_idesc_bf16(128, DP, 0, 1);
   auto issue_S = [&](int c) {  // thread 0 only
-    const uint32_t kb = s0 + (c & 1) * C::kStage;
+    const uint32_t kb = s0 + (c % C::kNSt) * C::kStage;
     tc_fence_after();
 #pragma unroll
     for (int kk = 0; kk < DP / 16; ++kk)
@@ -104,8 +106,7 @@ __global__ void __launch_bounds__(128, 4)
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     if (BIAS) tma_prefetch_desc(&tm_b);
-    load_chunk(0);
-    if (nc > 1) load_chunk(1);
+    for (int c = 0; c < C::kNSt && c < nc; ++c) load_chunk(c);
   }
   {
     uint32_t qrow[DP / 2], gpk[DP / 2];
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(128, 4)
   const uint64_t log2e2 = f2_pack(kLog2e, kLog2e);
   float m_ref = -INFINITY, l_run = 0.f;  // natural-log units
   for (int c = 0; c < nc; ++c) {
-    const int st = c & 1;
+    const int st = c % C::kNSt;
     const uint32_t sb = s0 + st * C::kStage;
     uint32_t mw0 = ~0u, mw1 = ~0u;
     if (!all_kept) {
@@ -276,8 +277,8 @@ __global__ void __launch_bounds__(128, 4)
       if (c + 1 < nc) {
         // S_{c+1} overwrites the P columns: wait for PV_c, which also frees stage `st`
         mbar_wait(bar_o, c & 1);
-        if (c + 2 < nc) load_chunk(c + 2);
-        mbar_wait(bar_kv0 + 8 * ((c + 1) & 1), ((c + 1) >> 1) & 1);
+        if (c + C::kNSt < nc) load_chunk(c + C::kNSt);
+        mbar_wait(bar_kv0 + 8 * ((c + 1) % C::kNSt), ((c + 1) / C::kNSt) & 1);
         issue_S(c + 1);
       }
     }
