@@ -51,6 +51,21 @@ def run(args, metric):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # the whole DAP block (attention calls + NCCL exchanges) as one CUDA graph (PAPER.md L264:
+    # graphs remove the per-launch CPU overhead that DAP exposes); NCCL supports stream capture
+    graph = None
+    if not getattr(args, "no_graph", False):
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            step()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
     from bench import ClockSampler  # noqa: E402  (repo root is on sys.path under bench.py)
     clocks = ClockSampler(local)
@@ -67,7 +82,10 @@ def run(args, metric):
             flush.zero_()
         comm.barrier()  # stragglers show up as their own time
         ev[s][0].record(stream)
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
         ev[s][1].record(stream)
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
@@ -79,6 +97,11 @@ def run(args, metric):
     flops = dap.block_flops(n_seq, n_res)
     # our kernels in the timed region: the attention core's launches (C ABI count) + one
     # pack/unpack per transpose when N > 1 (NCCL's own kernels are library code, not counted)
+    if graph is not None:  # replays do not pass through the binding: count one eager step
+        attn.launches = 0
+        step()
+        torch.cuda.synchronize()
+        attn.launches *= args.steps
     launches = attn.launches + (8 * args.steps if world > 1 else 0)
     e2e = _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops)
     if rank == 0:
@@ -91,7 +114,8 @@ def run(args, metric):
                        "parallelism": f"dap{world}", "local_shapes": dap.plan(world, n_seq, n_res),
                        "l2": "flushed (256 MB write) before every timed step" if not args.no_flush
                        else "warm",
-                       "collectives_per_block": {"a2a": 8, "allgather": 3, "reduce_scatter": 3}},
+                       "collectives_per_block": {"a2a": 8, "allgather": 3, "reduce_scatter": 3},
+                       "launch": "CUDA graph of the step" if graph is not None else "eager"},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
