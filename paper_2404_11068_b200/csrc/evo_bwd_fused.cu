@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(384, 1)
         keep = keep_next != 0u;
         keep_next = load_keep(b + 1);
       }
-      const bool rec = tid == 0 && j < 256;
+      const bool rec = (tid == 0 || tid == 128) && j < 256;
       if (rec) DBG(j * 8 + 0);
       mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
       if (rec) DBG(j * 8 + 1);

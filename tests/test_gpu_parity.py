@@ -115,3 +115,13 @@ def test_bf16_parity_pair_mode(monkeypatch, bias_t):
     errs, _, _ = run_case(3, 2, 256, 256, 32, seed=5, bias="shared", bias_t=bias_t, gate=True,
                           mask="prefix", mask_t=False, layout="blhd")
     _assert(errs, torch.bfloat16, f"pair mode bias_t={bias_t}")
+
+
+@pytest.mark.parametrize("B,H,L,bias", [(64, 8, 64, None), (64, 8, 32, None), (40, 2, 256, "shared"),
+                                        (200, 1, 128, "shared")])
+def test_bf16_parity_many_batch_rows(B, H, L, bias):
+    """Several batch rows per fused-backward CTA (batch chunks > 1): the per-row dK/dV drains,
+    the cross-row Σ_b dSᵀ and the K/V ring reuse."""
+    errs, _, _ = run_case(B, H, L, L, 32, seed=3, bias=bias, gate=True, mask="prefix",
+                          mask_t=False, layout="blhd")
+    _assert(errs, torch.bfloat16, f"B={B} H={H} L={L} bias={bias}")
