@@ -450,11 +450,55 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     };
+    // Split drains (default, no pair mode): group 0 drains dK/dV at a new batch row, group 1 the
+    // dQ part of the previous query tile, so the two groups share the drain work and group 0's
+    // dK/dV release (which gates the gradient issuer) is not queued behind the dQ store.
+    auto drain_kv = [&](int bk, bool release_kv) {  // group 0
+      if (tid == 0) bulk_wait_group_read0();
+      named_bar_sync(2, 128);
+      uint32_t r[DP];
+      tmem_ld_cols(tdK + lane_base, r);
+      tmem_wait_ld();
+      stage_bf16(s0 + C::oStK, r, a.scale);
+      tmem_ld_cols(tdV + lane_base, r);
+      tmem_wait_ld();
+      if (release_kv) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_dkvfree);
+      }
+      stage_bf16(s0 + C::oStV, r, 1.f);
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (tid == 0) {
+        tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
+        tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
+        bulk_commit_group();
+      }
+    };
+    auto drain_q = [&](int bq, int q0) {  // group 1
+      if (tid == 128) bulk_wait_group_read0();
+      named_bar_sync(3, 128);
+      uint32_t r[DP];
+      tmem_ld_cols(tdQ + lane_base, r);
+      tmem_wait_ld();
+      if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
+      else stage_f32(s0 + C::oStQ, r);
+      fence_proxy_async_smem();
+      named_bar_sync(3, 128);
+      if (tid == 128) {
+        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
+        bulk_commit_group();
+      }
+    };
     // hard-mask bit of this thread's key for batch row b (prefetched one batch row ahead)
     auto load_keep = [&](int b) -> uint32_t {
       if (kglob >= a.Lk || b >= a.B) return 0u;
       return a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kglob * a.mask_s1] : 1u;
     };
+    uint32_t pd_off[4];  // this thread's row of a [128][32] bf16 SW64 tile: 4 chunk offsets
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pd_off[e] = swz_offset(row, e, 64);
     uint32_t keep_next = load_keep(b0);
     bool keep = false;
     int bi = 0, t = 0, s = g;  // this group's sub-tiles: j = g, g+2, ...; j = ((bi*nq)+t)*4 + s
@@ -466,10 +510,7 @@ __global__ void __launch_bounds__(384, 1)
         keep = keep_next != 0u;
         keep_next = load_keep(b + 1);
       }
-      const bool rec = (tid == 0 || tid == 128) && j < 256;
-      if (rec) DBG(j * 8 + 0);
       mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
-      if (rec) DBG(j * 8 + 1);
       tc_fence_after();
       uint32_t rs[32], rd[32];
       {
@@ -481,7 +522,6 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_sfree + 8 * g);
-      if (rec) DBG(j * 8 + 2);
       mbar_wait(bar_in + 8 * st, (T >> 1) & 1);  // lse2 / D of this query tile visible
       const uint32_t vbase = s0 + C::oVec + st * 1024 + s * 32 * 4;
       const int qcol = t * 128 + s * 32;  // first query of this sub-tile
@@ -536,12 +576,10 @@ __global__ void __launch_bounds__(384, 1)
         }
         tmem_st32(tDB + lane_base + qcol, acc);
       }
-      if (rec) DBG(j * 8 + 3);
       // before overwriting: Pᵀ slot g is read by dV(j-2); the dSᵀ blocks of the previous tile by
       // its dQ MMA (each group checks at its first sub-tile of a tile)
       if (j >= 2) mbar_wait(bar_mm + 8 * g, ((j - 2) >> 1) & 1);
       if (s == g && T > 0) mbar_wait(bar_dq, (T - 1) & 1);
-      if (rec) DBG(j * 8 + 4);
       tc_fence_after();
       const bool drain_now = g == 0 && s == 0 && j > 0;
       // Pᵀ (slot g) and dSᵀ (block s) rows: this thread's key row, 32 queries = 4 x 16 B, SW64
@@ -549,9 +587,8 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t pb = s0 + C::oP + g * 8192, db = s0 + C::oDS + s * 8192;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t off = swz_offset(row, e, 64);
-          st_shared_v4(pb + off, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-          st_shared_v4(db + off, dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
+          st_shared_v4(pb + pd_off[e], pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          st_shared_v4(db + pd_off[e], dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
         }
       }
       if (BIAS) tmem_wait_st();
@@ -559,8 +596,13 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_ps + 8 * g);
-      if (rec) DBG(j * 8 + 5);
-      if (drain_now) {  // group 0: the previous query tile's dQ part (+ dK/dV at a new row)
+      if (!a.pairx) {
+        if (g == 0 && s == 0 && j > 0 && t == 0) drain_kv(b - 1, true);
+        if (g == 1 && s == 1 && T > 0) {
+          const int Tp = T - 1;
+          drain_q(b0 + Tp / nq, (Tp % nq) * 128);
+        }
+      } else if (drain_now) {  // pair mode: group 0 drains dQ (exchange) and dK/dV
         const int Tp = T - 1;
         drain(b0 + Tp / nq, (Tp % nq) * 128, t == 0, b - 1, true, a.pairx ? 1 : 0, Tp);
       } else if (a.pairx && g == 0 && s == 2 && T > 0) {  // pair: finish the previous tile's dQ
@@ -573,8 +615,19 @@ __global__ void __launch_bounds__(384, 1)
         if (++t == nq) { t = 0; ++bi; }
       }
     }
-    // ---- tail (group 0): last dQ part and last dK/dV; then both groups write Σ_b dSᵀ
-    if (g == 0) {
+    // ---- tail: last dQ part (group 1) and last dK/dV (group 0); then both write Σ_b dSᵀ
+    if (!a.pairx) {
+      const int Tl = (J >> 2) - 1;
+      mbar_wait(bar_dq, Tl & 1);
+      tc_fence_after();
+      if (g == 0) {
+        drain_kv(b0 + nb - 1, false);
+        if (tid == 0) bulk_wait_group0();
+      } else {
+        drain_q(b0 + Tl / nq, (Tl % nq) * 128);
+        if (tid == 128) bulk_wait_group0();
+      }
+    } else if (g == 0) {
       const int Tl = (J >> 2) - 1;
       mbar_wait(bar_dq, Tl & 1);
       tc_fence_after();
