@@ -548,14 +548,21 @@ __global__ void __launch_bounds__(384, 1)
           x = f2_fma(((uint64_t)rs[i + 1] << 32) | rs[i], sl2, x);
           float x0, x1;
           f2_unpack(x, x0, x1);
-          float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
-          if (!keep) { p0 = 0.f; p1 = 0.f; }
+          const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
           const uint64_t p2 = f2_pack(p0, p1);
           const uint64_t dd = f2_mul(p2, f2_add(((uint64_t)rd[i + 1] << 32) | rd[i], nd2));
           f2_unpack(dd, ds[i], ds[i + 1]);
           pk[i / 2] = pack_bf16(p0, p1);
           dk2[i / 2] = pack_bf16(ds[i], ds[i + 1]);
         }
+      }
+      // hard mask (R5): a masked key row has P = dS = 0.  The key is this thread's row, so the
+      // fix-up is per thread and skipped by whole warps in the common all-kept case
+      if (__any_sync(0xffffffffu, !keep) && !keep) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) { pk[i] = 0u; dk2[i] = 0u; }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ds[i] = 0.f;
       }
       if (BIAS) {  // Σ_b dSᵀ in TMEM (this thread's lane, this sub-tile's 32 query columns)
         uint32_t acc[32];
