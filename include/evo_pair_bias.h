@@ -25,7 +25,8 @@
  * DAP storage [L, H, L].  γ, β: [C] fp32; W: [C][H] fp32 row-major; mean, rstd: [Li·Lj] fp32
  * (row r = i·Lj + j), written by the forward and read by the backward; dz: bf16 with z_str.
  *
- * Supported: C in {32, 64, 128, 256}, 1 <= H <= 16, eps > 0.  Conventions as evo_attn.h: device
+ * Supported: C in {32, 64, 128, 256}, H in {4, 8, 16} (AF2: 8 for MSA row, 4 for triangle
+ * attention), eps > 0.  Conventions as evo_attn.h: device
  * pointers, 16-byte-aligned tensors, asynchronous on `stream`, errors returned (EVO_E_*), details
  * in evo_last_error_detail(), no allocation on the hot path (workspace from the caller).
  */
@@ -44,7 +45,7 @@ extern "C" {
 typedef struct {
   int64_t Li, Lj;       /* pair rows: i extent, j extent                              */
   int32_t C;            /* channels c_z: 32, 64, 128 or 256                            */
-  int32_t H;            /* heads, 1..16                                                */
+  int32_t H;            /* heads: 4, 8 or 16                                           */
   float eps;            /* LayerNorm epsilon, > 0 (AF2: 1e-5)                          */
   int64_t z_str[3];     /* element strides of z / dz for (i, j, c); c must be 1        */
   int64_t b_str[3];     /* element strides of bias / dbias for (h, i, j)               */

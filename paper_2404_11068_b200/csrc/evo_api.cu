@@ -16,6 +16,11 @@
 namespace {
 
 thread_local std::string g_detail;
+}  // namespace
+namespace evo {
+void set_error_detail(const char* msg) { g_detail = msg; }
+}  // namespace evo
+namespace {
 thread_local int g_launches = 0;
 constexpr int kNumSMs = 148;  // B200; fixes the dbias batch chunking (workspace is a pure
                               // function of the descriptor)

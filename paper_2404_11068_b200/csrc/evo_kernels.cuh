@@ -4,6 +4,9 @@
 
 namespace evo {
 
+// sets the thread-local text evo_last_error_detail() returns (evo_api.cu)
+void set_error_detail(const char* msg);
+
 constexpr int kMaxMaskWords = 512;  // Lk <= 16384
 constexpr int kMaxLk = kMaxMaskWords * 32;
 

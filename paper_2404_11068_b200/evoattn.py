@@ -50,6 +50,15 @@ class Desc(ctypes.Structure):
     ]
 
 
+class PairBiasDesc(ctypes.Structure):
+    """Mirror of evo_pair_bias_desc_t (include/evo_pair_bias.h)."""
+    _fields_ = [
+        ("Li", ctypes.c_int64), ("Lj", ctypes.c_int64), ("C", ctypes.c_int32),
+        ("H", ctypes.c_int32), ("eps", ctypes.c_float),
+        ("z_str", ctypes.c_int64 * 3), ("b_str", ctypes.c_int64 * 3),
+    ]
+
+
 def lib_path() -> str:
     return _LIB_PATH
 
@@ -84,6 +93,13 @@ def load():
             lib.evo_trace_count.restype = i32
             lib.evo_trace_label.argtypes = [i32]
             lib.evo_trace_label.restype = ctypes.c_char_p
+            pdp = ctypes.POINTER(PairBiasDesc)
+            lib.evo_pair_bias_fwd.argtypes = [pdp] + [vp] * 8
+            lib.evo_pair_bias_fwd.restype = i32
+            lib.evo_pair_bias_bwd_workspace_bytes.argtypes = [pdp]
+            lib.evo_pair_bias_bwd_workspace_bytes.restype = sz
+            lib.evo_pair_bias_bwd.argtypes = [pdp] + [vp] * 12 + [sz, vp]
+            lib.evo_pair_bias_bwd.restype = i32
             _lib = lib
     return _lib
 
@@ -248,3 +264,51 @@ class EvoAttentionFunction(torch.autograd.Function):
 def evo_attention(q, k, v, bias=None, g=None, mask=None, scale=None):
     """Differentiable gated pair-bias attention (bf16 or fp32-verification inputs)."""
     return EvoAttentionFunction.apply(q, k, v, bias, g, mask, scale)
+
+
+# ----------------------------------------------------------------------------- pair-bias side path
+def _pb_desc(z, W, eps, b):
+    d = PairBiasDesc()
+    d.Li, d.Lj, d.C = z.shape
+    d.H = W.shape[1]
+    d.eps = float(eps)
+    d.z_str = (ctypes.c_int64 * 3)(*z.stride())
+    d.b_str = (ctypes.c_int64 * 3)(*b.stride())
+    return d
+
+
+def pair_bias_fwd(z, gamma, beta, W, eps=1e-5, bias=None, stream=None):
+    """LayerNorm(z) + LinearNoBias into the head-major bias (include/evo_pair_bias.h).
+    z [Li, Lj, C] bf16 (channel unit-stride); gamma, beta [C] fp32; W [C, H] fp32 contiguous.
+    ``bias``: optional bf16 output view [H, Li, Lj] with any strides (e.g. a transposed or DAP
+    layout); default a new contiguous [H, Li, Lj].  Returns (bias, mean, rstd)."""
+    Li, Lj, C = z.shape
+    H = W.shape[1]
+    if bias is None:
+        bias = torch.empty((H, Li, Lj), dtype=torch.bfloat16, device=z.device)
+    mean = torch.empty((Li, Lj), dtype=torch.float32, device=z.device)
+    rstd = torch.empty_like(mean)
+    d = _pb_desc(z, W, eps, bias)
+    _check(load().evo_pair_bias_fwd(ctypes.byref(d), _ptr(z), _ptr(gamma), _ptr(beta),
+                                    _ptr(W.contiguous()), _ptr(bias), _ptr(mean), _ptr(rstd),
+                                    _stream(stream)))
+    return bias, mean, rstd
+
+
+def pair_bias_bwd(z, gamma, beta, W, mean, rstd, dbias, eps=1e-5, workspace=None, stream=None):
+    """Backward of pair_bias_fwd given dbias [H, Li, Lj] fp32 (any strides).  Returns dict
+    dz (bf16, z's strides), dgamma, dbeta [C], dW [C, H] (fp32)."""
+    d = _pb_desc(z, W, eps, dbias)
+    need = int(load().evo_pair_bias_bwd_workspace_bytes(ctypes.byref(d)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=z.device)
+    dz = _alloc_like(z)
+    C, H = W.shape
+    dgamma = torch.empty(C, dtype=torch.float32, device=z.device)
+    dbeta = torch.empty_like(dgamma)
+    dW = torch.empty((C, H), dtype=torch.float32, device=z.device)
+    _check(load().evo_pair_bias_bwd(ctypes.byref(d), _ptr(z), _ptr(gamma), _ptr(beta),
+                                    _ptr(W.contiguous()), _ptr(mean), _ptr(rstd), _ptr(dbias),
+                                    _ptr(dz), _ptr(dgamma), _ptr(dbeta), _ptr(dW),
+                                    _ptr(workspace), need, _stream(stream)))
+    return {"dz": dz, "dgamma": dgamma, "dbeta": dbeta, "dW": dW}

@@ -43,6 +43,42 @@ def test_dap_library_exports(tmp_path):
         assert hasattr(dl, n), f"libevodap.so does not export {n}"
 
 
+def test_pair_bias_exports_and_descriptor(lib, tmp_path):
+    for n in _declared("evo_pair_bias.h"):
+        assert hasattr(lib, n), f"libevoattn.so does not export {n}"
+    from paper_2404_11068_b200.evoattn import PairBiasDesc
+    fields = [f[0] for f in PairBiasDesc._fields_]
+    src = tmp_path / "pb.c"
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof(evo_pair_bias_desc_t, {f}));' for f in fields)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "evo_pair_bias.h"\n'
+                   'int main(void){printf("size %zu\\n", sizeof(evo_pair_bias_desc_t));' + body + "}")
+    exe = tmp_path / "pb"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    assert int(out["size"]) == ctypes.sizeof(PairBiasDesc)
+    for f in fields:
+        assert int(out[f]) == getattr(PairBiasDesc, f).offset, f
+
+
+def test_pair_bias_validation(lib):
+    from paper_2404_11068_b200.evoattn import PairBiasDesc
+    d = PairBiasDesc()
+    d.Li, d.Lj, d.C, d.H, d.eps = 4, 4, 96, 4, 1e-5
+    d.z_str = (ctypes.c_int64 * 3)(4 * 96, 96, 1)
+    d.b_str = (ctypes.c_int64 * 3)(16, 4, 1)
+    p = ctypes.c_void_p(16)
+    lib.evo_pair_bias_fwd.restype = ctypes.c_int
+    rc = lib.evo_pair_bias_fwd(ctypes.byref(d), p, p, p, p, p, p, p, None)
+    assert rc == 4  # EVO_E_UNSUPPORTED (C = 96)
+    d.C, d.H = 128, 5
+    assert lib.evo_pair_bias_fwd(ctypes.byref(d), p, p, p, p, p, p, p, None) == 4
+    d.H, d.eps = 4, 0.0
+    assert lib.evo_pair_bias_fwd(ctypes.byref(d), p, p, p, p, p, p, p, None) == 1
+    d.eps = 1e-5
+    d.z_str = (ctypes.c_int64 * 3)(4 * 128, 128, 2)
+    assert lib.evo_pair_bias_fwd(ctypes.byref(d), p, p, p, p, p, p, p, None) == 3
+
+
 def test_descriptor_layout_matches_c(tmp_path):
     from paper_2404_11068_b200.evoattn import Desc
     src = tmp_path / "sz.c"
