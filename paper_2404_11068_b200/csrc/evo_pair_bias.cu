@@ -6,10 +6,8 @@
 // column reduction) with no atomics.  HBM-bound: z is read once (fwd) / twice (fwd + bwd) and
 // dz written once.
 //
-// Mapping: TPR = max(1, C/64) threads per pair row, each holding C/TPR channels (≤ 64) of the
-// row in registers; rows of a warp are consecutive along j, so the z loads (16 B per thread)
-// and the per-head bias stores (consecutive j) are coalesced.  W, γ, β live in shared memory
-// (broadcast reads).
+// Mapping: one warp per pair row at a time (lanes across channels), 64 consecutive rows per warp;
+// see the kernels below.
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -37,160 +35,233 @@ struct PbArgs {
   int rows_per_block;
 };
 
-template <int CP>  // channels per thread (C / TPR)
-EVO_DEV void load_row(const __nv_bfloat16* p, float (&v)[CP]) {
-#pragma unroll
-  for (int c = 0; c < CP; c += 8) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p + c);
+// Warp per pair row, lanes across channels (NC = C/32 channels per lane, 8-byte-aligned runs):
+// a row is one coalesced 2·C-byte read; the per-lane W slice (NC x H) stays in registers for the
+// whole kernel; reductions over the row are warp butterflies (every lane ends with the sum).
+// A warp walks ROWS_PER_WARP consecutive rows (consecutive j), so the per-head bias values of
+// 32 rows land in 32 lanes and leave as coalesced stores.
+constexpr int kFwdRowsPerWarp = 4;   // forward: rows per warp (all loads issued up front)
+constexpr int kRowsPerWarp = 16;     // backward: rows per warp (amortises the dW/dγ/dβ partials)
+
+template <int NC>
+EVO_DEV void load_nc(const __nv_bfloat16* p, float (&v)[NC]) {
+  if constexpr (NC == 1) {
+    v[0] = __bfloat162float(*p);
+  } else if constexpr (NC == 2) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = bf16_lo(u); v[1] = bf16_hi(u);
+  } else if constexpr (NC == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = bf16_lo(u.x); v[1] = bf16_hi(u.x); v[2] = bf16_lo(u.y); v[3] = bf16_hi(u.y);
+  } else {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      v[c + 2 * e] = bf16_lo(w[e]);
-      v[c + 2 * e + 1] = bf16_hi(w[e]);
-    }
+    for (int e = 0; e < 4; ++e) { v[2 * e] = bf16_lo(w[e]); v[2 * e + 1] = bf16_hi(w[e]); }
   }
 }
 
-template <int TPR>
-EVO_DEV float group_sum(float x) {  // sum over the TPR consecutive lanes of one row
+// Reduce-scatter of H per-lane partials across the warp: log2(H) halving steps (lanes with the
+// offset bit set keep the upper half) then full butterflies; H - 1 + (5 - log2 H) shuffles
+// instead of 5·H.  Afterwards lane l holds the full sum of head (l >> (5 - log2 H)).
+template <int H>
+EVO_DEV float warp_reduce_scatter(float (&v)[H], int lane) {
 #pragma unroll
-  for (int o = 1; o < TPR; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  for (int off = 16, n = H; off >= 1; off >>= 1) {
+    if (n > 1) {
+      const int half = n / 2;
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int t = 0; t < H / 2; ++t) {
+        if (t < half) {
+          const float send = up ? v[t] : v[t + half];
+          const float keep = up ? v[t + half] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      n = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+  return v[0];
+}
+
+EVO_DEV float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
 
 // ------------------------------------------------------------------ forward
-template <int C, int TPR, int H>
+template <int C, int H>
 __global__ void __launch_bounds__(256) pair_bias_fwd_kernel(const PbArgs a) {
-  constexpr int CP = C / TPR;
-  __shared__ float sW[C * H], sG[C], sB[C];
-  for (int i = threadIdx.x; i < C * H; i += blockDim.x) sW[i] = a.W[i];
-  for (int i = threadIdx.x; i < C; i += blockDim.x) { sG[i] = a.gamma[i]; sB[i] = a.beta[i]; }
-  __syncthreads();
+  constexpr int NC = C / 32;
+  const int lane = threadIdx.x & 31;
   const int64_t nrows = a.Li * a.Lj;
-  const int sub = threadIdx.x % TPR;
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPR;
-  const bool valid = r < nrows;
-  const int64_t i = valid ? r / a.Lj : 0, j = valid ? r % a.Lj : 0;
-  float v[CP];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r0 = warp * kFwdRowsPerWarp;
+  if (r0 >= nrows) return;
+  float w[NC][H], gm[NC], bt[NC];
 #pragma unroll
-  for (int c = 0; c < CP; ++c) v[c] = 0.f;
-  if (valid) load_row<CP>(a.z + i * a.z_si + j * a.z_sj + sub * CP, v);
-  float s = 0.f, ss = 0.f;  // single pass: Σz, Σz²
+  for (int c = 0; c < NC; ++c) {
+    const int cc = lane * NC + c;
+    gm[c] = a.gamma[cc];
+    bt[c] = a.beta[cc];
 #pragma unroll
-  for (int c = 0; c < CP; ++c) { s += v[c]; ss = fmaf(v[c], v[c], ss); }
-  s = group_sum<TPR>(s);
-  ss = group_sum<TPR>(ss);
-  const float mean = s / C;
-  const float var = fmaxf(ss / C - mean * mean, 0.f);
-  const float rstd = rsqrtf(var + a.eps);
-  float dot[H];
+    for (int h = 0; h < H; ++h) w[c][h] = a.W[cc * H + h];
+  }
+  // rows r0.. are consecutive: one division per warp, then (i, j) steps (no 64-bit division per row)
+  int64_t ri[kFwdRowsPerWarp], rj[kFwdRowsPerWarp];
+  {
+    int64_t i = r0 / a.Lj, j = r0 - i * a.Lj;
 #pragma unroll
-  for (int h = 0; h < H; ++h) dot[h] = 0.f;
+    for (int k = 0; k < kFwdRowsPerWarp; ++k) {
+      ri[k] = i; rj[k] = j;
+      if (++j == a.Lj) { j = 0; ++i; }
+    }
+  }
+  float v[kFwdRowsPerWarp][NC];  // all rows' loads in flight first
 #pragma unroll
-  for (int c = 0; c < CP; ++c) {
-    const int cc = sub * CP + c;
-    const float y = fmaf((v[c] - mean) * rstd, sG[cc], sB[cc]);
-#pragma unroll
-    for (int h = 0; h < H; ++h) dot[h] = fmaf(y, sW[cc * H + h], dot[h]);
+  for (int k = 0; k < kFwdRowsPerWarp; ++k) {
+    const bool ok = r0 + k < nrows;
+    load_nc<NC>(a.z + (ok ? ri[k] : ri[0]) * a.z_si + (ok ? rj[k] : rj[0]) * a.z_sj + lane * NC, v[k]);
   }
 #pragma unroll
-  for (int h = 0; h < H; ++h) dot[h] = group_sum<TPR>(dot[h]);
-  if (valid && sub == 0) {
+  for (int k = 0; k < kFwdRowsPerWarp; ++k) {
+    const int64_t r = r0 + k;
+    float s = 0.f, ss = 0.f;  // one pass: Σz, Σz²
 #pragma unroll
-    for (int h = 0; h < H; ++h)
-      a.bias[h * a.b_sh + i * a.b_si + j * a.b_sj] = __float2bfloat16_rn(dot[h]);
-    a.mean[r] = mean;
-    a.rstd[r] = rstd;
+    for (int c = 0; c < NC; ++c) { s += v[k][c]; ss = fmaf(v[k][c], v[k][c], ss); }
+    s = warp_sum(s);
+    ss = warp_sum(ss);
+    const float mean = s / C;
+    const float rstd = rsqrtf(fmaxf(ss / C - mean * mean, 0.f) + a.eps);
+    float dot[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) dot[h] = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const float y = fmaf((v[k][c] - mean) * rstd, gm[c], bt[c]);
+#pragma unroll
+      for (int h = 0; h < H; ++h) dot[h] = fmaf(y, w[c][h], dot[h]);
+    }
+    constexpr int kSh = H == 4 ? 3 : (H == 8 ? 2 : 1);  // lane >> kSh = head of the sum
+    const float mine = warp_reduce_scatter<H>(dot, lane);
+    if (r < nrows) {
+      const int64_t i = ri[k], j = rj[k];
+      if ((lane & ((1 << kSh) - 1)) == 0)
+        a.bias[(lane >> kSh) * a.b_sh + i * a.b_si + j * a.b_sj] = __float2bfloat16_rn(mine);
+      if (lane == 0) { a.mean[r] = mean; a.rstd[r] = rstd; }
+    }
   }
 }
 
 // ------------------------------------------------------------------ backward
-// Block = rows_per_block rows (RB = 8192 / C).  Phase 1 (TPR threads per row): dz, and the
-// row's ẑ, y, dy into shared memory; phase 2 (thread per output): the block's partial of dW, dγ,
-// dβ as plain sums over its rows, in row order.
-template <int C, int TPR, int H>
+// Same warp-per-row walk; every lane accumulates the parameter gradients of its NC channels over
+// the warp's rows in registers (dW NC x H, dγ, dβ), the block's 8 warps are summed in a fixed
+// order through shared memory into one partial per block, and pair_bias_reduce_kernel sums the
+// block partials column by column (the paper's two-step reduction; no atomics, deterministic).
+template <int C, int H>
 __global__ void __launch_bounds__(256) pair_bias_bwd_kernel(const PbArgs a) {
-  constexpr int CP = C / TPR;
-  constexpr int RB = 8192 / C;
-  extern __shared__ float sm[];
-  float* sY = sm;                 // [RB][C]
-  float* sDY = sY + RB * C;       // [RB][C]
-  float* sZH = sDY + RB * C;      // [RB][C]
-  float* sDB = sZH + RB * C;      // [RB][H]
-  float* sW = sDB + RB * H;       // [C][H]
-  float* sG = sW + C * H;         // [C]
-  float* sB = sG + C;             // [C]
-  for (int t = threadIdx.x; t < C * H; t += blockDim.x) sW[t] = a.W[t];
-  for (int t = threadIdx.x; t < C; t += blockDim.x) { sG[t] = a.gamma[t]; sB[t] = a.beta[t]; }
-  __syncthreads();
+  constexpr int NC = C / 32;
+  constexpr int NOUT = C * H + 2 * C;
+  extern __shared__ float red_raw[];
+  float (*red)[NOUT] = reinterpret_cast<float (*)[NOUT]>(red_raw);  // [8 warps][NOUT]
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
   const int64_t nrows = a.Li * a.Lj;
-  const int sub = threadIdx.x % TPR;
-  const int rl = threadIdx.x / TPR;  // row within the block
-  const int64_t r = (int64_t)blockIdx.x * RB + rl;
-  const bool valid = r < nrows;
-  const int64_t i = valid ? r / a.Lj : 0, j = valid ? r % a.Lj : 0;
-  float v[CP];
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + wv) * kRowsPerWarp;
+  float w[NC][H], gm[NC], bt[NC];
 #pragma unroll
-  for (int c = 0; c < CP; ++c) v[c] = 0.f;
-  if (valid) load_row<CP>(a.z + i * a.z_si + j * a.z_sj + sub * CP, v);
-  const float mean = valid ? a.mean[r] : 0.f, rstd = valid ? a.rstd[r] : 0.f;
-  float db[H];
+  for (int c = 0; c < NC; ++c) {
+    const int cc = lane * NC + c;
+    gm[c] = a.gamma[cc];
+    bt[c] = a.beta[cc];
 #pragma unroll
-  for (int h = 0; h < H; ++h) db[h] = valid ? a.dbias[h * a.b_sh + i * a.b_si + j * a.b_sj] : 0.f;
-  if (sub == 0) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) sDB[rl * H + h] = db[h];
+    for (int h = 0; h < H; ++h) w[c][h] = a.W[cc * H + h];
   }
-  float g[CP];
-  float sg = 0.f, sgz = 0.f;
+  float dw[NC][H], dg[NC], dbt[NC];
 #pragma unroll
-  for (int c = 0; c < CP; ++c) {
-    const int cc = sub * CP + c;
-    const float zh = (v[c] - mean) * rstd;
-    float dy = 0.f;
+  for (int c = 0; c < NC; ++c) {
+    dg[c] = 0.f;
+    dbt[c] = 0.f;
 #pragma unroll
-    for (int h = 0; h < H; ++h) dy = fmaf(db[h], sW[cc * H + h], dy);
-    sY[rl * C + cc] = fmaf(zh, sG[cc], sB[cc]);
-    sDY[rl * C + cc] = dy;
-    sZH[rl * C + cc] = zh;
-    g[c] = dy * sG[cc];
-    sg += g[c];
-    sgz = fmaf(g[c], zh, sgz);
-    v[c] = zh;
+    for (int h = 0; h < H; ++h) dw[c][h] = 0.f;
   }
-  sg = group_sum<TPR>(sg) / C;
-  sgz = group_sum<TPR>(sgz) / C;
-  if (valid) {
-    __nv_bfloat16* dp = a.dz + i * a.z_si + j * a.z_sj + sub * CP;
+  for (int rb = 0; rb < kRowsPerWarp; rb += 32) {
+    // dbias, mean, rstd of up to 32 rows: one coalesced load per head, then broadcast per row
+    float dbl[H], ml = 0.f, rl = 0.f;
+    int64_t i0 = (r0 + rb) / a.Lj, j0 = (r0 + rb) - ((r0 + rb) / a.Lj) * a.Lj;  // first row
+    {
+      const int64_t r = r0 + rb + lane;
+      const bool ok = r < nrows && lane < kRowsPerWarp;
+      const int64_t i = ok ? r / a.Lj : 0, j = ok ? r % a.Lj : 0;
 #pragma unroll
-    for (int c = 0; c < CP; c += 8) {
-      float d[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) d[e] = rstd * (g[c + e] - sg - v[c + e] * sgz);
-      uint4 u;
-      u.x = pack_bf16(d[0], d[1]); u.y = pack_bf16(d[2], d[3]);
-      u.z = pack_bf16(d[4], d[5]); u.w = pack_bf16(d[6], d[7]);
-      *reinterpret_cast<uint4*>(dp + c) = u;
+      for (int h = 0; h < H; ++h) dbl[h] = ok ? a.dbias[h * a.b_sh + i * a.b_si + j * a.b_sj] : 0.f;
+      if (ok) { ml = a.mean[r]; rl = a.rstd[r]; }
     }
+    for (int k = 0; k < 32 && rb + k < kRowsPerWarp; ++k) {
+      const int64_t r = r0 + rb + k;
+      if (r >= nrows) break;  // warp-uniform
+      const int64_t i = i0, j = j0;
+      if (++j0 == a.Lj) { j0 = 0; ++i0; }
+      float v[NC];
+      load_nc<NC>(a.z + i * a.z_si + j * a.z_sj + lane * NC, v);
+      const float mean = __shfl_sync(0xffffffffu, ml, k), rstd = __shfl_sync(0xffffffffu, rl, k);
+      float db[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) db[h] = __shfl_sync(0xffffffffu, dbl[h], k);
+      float zh[NC], g[NC], sg = 0.f, sgz = 0.f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        zh[c] = (v[c] - mean) * rstd;
+        const float y = fmaf(zh[c], gm[c], bt[c]);
+        float dy = 0.f;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          dy = fmaf(db[h], w[c][h], dy);
+          dw[c][h] = fmaf(y, db[h], dw[c][h]);
+        }
+        dg[c] = fmaf(dy, zh[c], dg[c]);
+        dbt[c] += dy;
+        g[c] = dy * gm[c];
+        sg += g[c];
+        sgz = fmaf(g[c], zh[c], sgz);
+      }
+      sg = warp_sum(sg) / C;
+      sgz = warp_sum(sgz) / C;
+      float d[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) d[c] = rstd * (g[c] - sg - zh[c] * sgz);
+      __nv_bfloat16* dp = a.dz + i * a.z_si + j * a.z_sj + lane * NC;
+      if constexpr (NC == 1) {
+        *dp = __float2bfloat16_rn(d[0]);
+      } else if constexpr (NC == 2) {
+        *reinterpret_cast<uint32_t*>(dp) = pack_bf16(d[0], d[1]);
+      } else if constexpr (NC == 4) {
+        *reinterpret_cast<uint2*>(dp) = make_uint2(pack_bf16(d[0], d[1]), pack_bf16(d[2], d[3]));
+      } else {
+        *reinterpret_cast<uint4*>(dp) = make_uint4(pack_bf16(d[0], d[1]), pack_bf16(d[2], d[3]),
+                                                   pack_bf16(d[4], d[5]), pack_bf16(d[6], d[7]));
+      }
+    }
+  }
+  // block partial: warp w's per-channel sums into red[w], then a fixed-order sum over warps
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int cc = lane * NC + c;
+#pragma unroll
+    for (int h = 0; h < H; ++h) red[wv][cc * H + h] = dw[c][h];
+    red[wv][C * H + cc] = dg[c];
+    red[wv][C * H + C + cc] = dbt[c];
   }
   __syncthreads();
-  const int nout = C * H + 2 * C;
-  const int64_t left = nrows - (int64_t)blockIdx.x * RB;
-  const int rows_here = left < RB ? (int)left : RB;
-  float* part = a.partial + (int64_t)blockIdx.x * nout;
-  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-    float acc = 0.f;
-    if (o < C * H) {  // dW[c][h] = Σ_rows y_c · dbias_h
-      const int c = o / H, h = o % H;
-      for (int q = 0; q < rows_here; ++q) acc = fmaf(sY[q * C + c], sDB[q * H + h], acc);
-    } else if (o < C * H + C) {  // dγ_c = Σ_rows dy_c · ẑ_c
-      const int c = o - C * H;
-      for (int q = 0; q < rows_here; ++q) acc = fmaf(sDY[q * C + c], sZH[q * C + c], acc);
-    } else {  // dβ_c = Σ_rows dy_c
-      const int c = o - C * H - C;
-      for (int q = 0; q < rows_here; ++q) acc += sDY[q * C + c];
-    }
-    part[o] = acc;
+  float* part = a.partial + (int64_t)blockIdx.x * NOUT;
+  for (int o = threadIdx.x; o < NOUT; o += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][o];
+    part[o] = t;
   }
 }
 
@@ -217,34 +288,34 @@ __global__ void __launch_bounds__(256) pair_bias_reduce_kernel(const float* __re
   }
 }
 
-template <int C, int TPR>
-static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
-  const int64_t threads = a.Li * a.Lj * TPR;
-  const unsigned grid = (unsigned)((threads + 255) / 256);
-#define EVO_PB_H(hh) \
-  if (a.H <= hh) { pair_bias_fwd_kernel<C, TPR, hh><<<grid, 256, 0, st>>>(a); return cudaGetLastError(); }
-  EVO_PB_H(4) EVO_PB_H(8) EVO_PB_H(16)
-#undef EVO_PB_H
-  return cudaErrorInvalidValue;
-}
+inline int64_t pb_warps(const PbArgs& a) { return (a.Li * a.Lj + kRowsPerWarp - 1) / kRowsPerWarp; }
 
-template <int C, int TPR, int H>
-static cudaError_t launch_bwd_ch(const PbArgs& a, cudaStream_t st) {
-  constexpr int RB = 8192 / C;
-  const size_t smem = (size_t)(3 * RB * C + RB * H + C * H + 2 * C) * 4;
-  auto k = pair_bias_bwd_kernel<C, TPR, H>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const unsigned grid = (unsigned)((a.Li * a.Lj + RB - 1) / RB);
-  k<<<grid, RB * TPR, smem, st>>>(a);
+template <int C>
+static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
+  const int64_t warps = (a.Li * a.Lj + kFwdRowsPerWarp - 1) / kFwdRowsPerWarp;
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  if (a.H == 4) pair_bias_fwd_kernel<C, 4><<<grid, 256, 0, st>>>(a);
+  else if (a.H == 8) pair_bias_fwd_kernel<C, 8><<<grid, 256, 0, st>>>(a);
+  else pair_bias_fwd_kernel<C, 16><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int C, int TPR>
+template <int C, int H>
+static cudaError_t launch_bwd_ch(const PbArgs& a, cudaStream_t st) {
+  const unsigned grid = (unsigned)((pb_warps(a) + 7) / 8);
+  auto k = pair_bias_bwd_kernel<C, H>;
+  constexpr size_t smem = 8 * (C * H + 2 * C) * 4;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int C>
 static cudaError_t launch_bwd_c(const PbArgs& a, cudaStream_t st) {
-  if (a.H <= 4) return launch_bwd_ch<C, TPR, 4>(a, st);
-  if (a.H <= 8) return launch_bwd_ch<C, TPR, 8>(a, st);
-  return launch_bwd_ch<C, TPR, 16>(a, st);
+  if (a.H == 4) return launch_bwd_ch<C, 4>(a, st);
+  if (a.H == 8) return launch_bwd_ch<C, 8>(a, st);
+  return launch_bwd_ch<C, 16>(a, st);
 }
 
 }  // namespace evo
@@ -286,21 +357,24 @@ evo::PbArgs make_args(const evo_pair_bias_desc_t* d) {
 
 cudaError_t launch_fwd(const evo::PbArgs& a, cudaStream_t st) {
   switch (a.C) {
-    case 32: return evo::launch_fwd_c<32, 1>(a, st);
-    case 64: return evo::launch_fwd_c<64, 1>(a, st);
-    case 128: return evo::launch_fwd_c<128, 2>(a, st);
-    default: return evo::launch_fwd_c<256, 4>(a, st);
+    case 32: return evo::launch_fwd_c<32>(a, st);
+    case 64: return evo::launch_fwd_c<64>(a, st);
+    case 128: return evo::launch_fwd_c<128>(a, st);
+    default: return evo::launch_fwd_c<256>(a, st);
   }
 }
 cudaError_t launch_bwd(const evo::PbArgs& a, cudaStream_t st) {
   switch (a.C) {
-    case 32: return evo::launch_bwd_c<32, 1>(a, st);
-    case 64: return evo::launch_bwd_c<64, 1>(a, st);
-    case 128: return evo::launch_bwd_c<128, 2>(a, st);
-    default: return evo::launch_bwd_c<256, 4>(a, st);
+    case 32: return evo::launch_bwd_c<32>(a, st);
+    case 64: return evo::launch_bwd_c<64>(a, st);
+    case 128: return evo::launch_bwd_c<128>(a, st);
+    default: return evo::launch_bwd_c<256>(a, st);
   }
 }
-int64_t bwd_blocks(const evo_pair_bias_desc_t* d) { return (d->Li * d->Lj + 8192 / d->C - 1) / (8192 / d->C); }
+int64_t bwd_blocks(const evo_pair_bias_desc_t* d) {
+  const int64_t warps = (d->Li * d->Lj + evo::kRowsPerWarp - 1) / evo::kRowsPerWarp;
+  return (warps + 7) / 8;
+}
 }  // namespace
 
 extern "C" {
