@@ -381,7 +381,18 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
   // kernel variant (A/B experiments only): "occ" (default), "ws", "v1"
   static const char* impl = getenv("EVO_FWD_IMPL") ? getenv("EVO_FWD_IMPL") : "occ";
   cudaError_t e;
-  if (!strcmp(impl, "occ")) {
+  if (!strcmp(impl, "pp") && dpad(d->D) <= 32) {
+    evo::FwdPpLaunch P;
+    memset(&P, 0, sizeof(P));
+    if (!make_x_map(&P.tm_q, q, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str) ||
+        (g && !make_x_map(&P.tm_g, g, dt, 2, d->B, d->H, d->Lq, d->D, d->g_str)) ||
+        !make_x_map(&P.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||
+        !make_x_map(&P.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 64) ||
+        (bm && !make_bias_map(&P.tm_b, d, bias, bm == 1 ? 128 : 64)))
+      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed (pp)");
+    P.args = a;
+    e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_pp_bf16(P, dpad(d->D), bm, st); });
+  } else if (!strcmp(impl, "occ") || !strcmp(impl, "pp")) {
     evo::FwdOccLaunch O;
     memset(&O, 0, sizeof(O));
     if (!make_x_map(&O.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||

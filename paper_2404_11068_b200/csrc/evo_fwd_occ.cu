@@ -31,7 +31,8 @@ struct OccCfg {
   // K/V(/bias) ring depth: 2 stages with a bias tile (smem-bound at 4 CTAs/SM), 4 without (long
   // key sequences otherwise expose the TMA latency)
   static constexpr int kNSt = BIAS ? 2 : 4;
-  static constexpr uint32_t kSmem = kNSt * kStage + 128;     // stages + barriers
+  static constexpr uint32_t oMask = kNSt * kStage + 128;     // 32-key hard-mask words
+  static constexpr uint32_t kSmem = oMask + kMaxMaskWords * 4;
   static constexpr uint32_t kTmemCols = DP <= 32 ? 128 : 256;
   static constexpr uint32_t cS = 0, cO = 64, cQ = DP <= 32 ? 96 : 128;
 };
@@ -108,6 +109,16 @@ __global__ void __launch_bounds__(128, 4)
     if (BIAS) tma_prefetch_desc(&tm_b);
     for (int c = 0; c < C::kNSt && c < nc; ++c) load_chunk(c);
   }
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + C::oMask);
+  const bool all_kept = a.mask == nullptr && (a.Lk & 63) == 0;
+  uint32_t keep_pre[4] = {0, 0, 0, 0};  // mask bytes of words w, w+4, w+8, w+12 (in flight)
+  if (!all_kept) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int kk = (w + 4 * x) * 32 + lane;
+      if (kk < a.Lk) keep_pre[x] = a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kk * a.mask_s1] : 1u;
+    }
+  }
   {
     uint32_t qrow[DP / 2], gpk[DP / 2];
     const __nv_bfloat16* qp = qptr + (int64_t)b * q_sb + (int64_t)h * q_sh + (int64_t)q * q_sl;
@@ -135,24 +146,32 @@ __global__ void __launch_bounds__(128, 4)
     tmem_st32(tG + lane_base, *reinterpret_cast<uint32_t(*)[32]>(gpk));
   }
   }
+  // hard-mask bits of this unit's batch row as 32-key words in smem (one pass instead of a
+  // dependent global load per chunk); the first words' loads were issued with the Q/G loads
+  if (!all_kept) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int wd = w + 4 * x;
+      if (wd < nc * 2) {
+        const uint32_t word = __ballot_sync(0xffffffffu, keep_pre[x] != 0);
+        if (lane == 0) smask[wd] = word;
+      }
+    }
+    for (int wd = w + 16; wd < nc * 2; wd += 4) {
+      const int kk = wd * 32 + lane;
+      const uint32_t keep = kk < a.Lk ? (a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kk * a.mask_s1] : 1u) : 0u;
+      const uint32_t word = __ballot_sync(0xffffffffu, keep != 0);
+      if (lane == 0) smask[wd] = word;
+    }
+  }
   tmem_wait_st();
   tc_fence_before();
-  __syncthreads();  // Q in TMEM
+  __syncthreads();  // Q in TMEM, mask words in smem
   if (tid == 0) {
     tc_fence_after();
     mbar_wait(bar_kv0, 0);
     issue_S(0);
   }
-
-  // mask bytes of this warp's view of chunk c: keys 64c + lane and 64c + 32 + lane
-  auto load_keep = [&](int c, uint32_t& r0, uint32_t& r1) {
-    const int k0 = c * 64 + lane, k1 = k0 + 32;
-    r0 = k0 < a.Lk ? (a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)k0 * a.mask_s1] : 1u) : 0u;
-    r1 = k1 < a.Lk ? (a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)k1 * a.mask_s1] : 1u) : 0u;
-  };
-  const bool all_kept = a.mask == nullptr && (a.Lk & 63) == 0;
-  uint32_t kn0 = 1, kn1 = 1;
-  if (!all_kept) load_keep(0, kn0, kn1);
 
   const uint64_t scale2 = f2_pack(a.scale, a.scale);
   const uint64_t log2e2 = f2_pack(kLog2e, kLog2e);
@@ -161,12 +180,7 @@ __global__ void __launch_bounds__(128, 4)
     const int st = c % C::kNSt;
     const uint32_t sb = s0 + st * C::kStage;
     uint32_t mw0 = ~0u, mw1 = ~0u;
-    if (!all_kept) {
-      const uint32_t r0 = kn0, r1 = kn1;
-      if (c + 1 < nc) load_keep(c + 1, kn0, kn1);
-      mw0 = __ballot_sync(0xffffffffu, r0 != 0);
-      mw1 = __ballot_sync(0xffffffffu, r1 != 0);
-    }
+    if (!all_kept) { mw0 = smask[2 * c]; mw1 = smask[2 * c + 1]; }
     mbar_wait(bar_s, c & 1);
     tc_fence_after();
     float x[64];

@@ -45,6 +45,12 @@ struct FwdOccLaunch {
   int64_t q_sb, q_sh, q_sl;
 };
 cudaError_t launch_fwd_occ_bf16(const FwdOccLaunch& L, int DP, int bias_mode, cudaStream_t st);
+// ping-pong persistent forward (evo_fwd_pp.cu): Q and G by TMA (128-row boxes), K/V 64-row boxes
+struct FwdPpLaunch {
+  CUtensorMap tm_q, tm_g, tm_k, tm_v, tm_b;
+  FwdArgs args;
+};
+cudaError_t launch_fwd_pp_bf16(const FwdPpLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
 // ------------------------------------------------------------------ backward (bf16)
 struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
