@@ -38,8 +38,54 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
         const int64_t orow = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl;
         const int64_t grow = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl;
         const int64_t arow = b * a.a_sb + h * a.a_sh + (int64_t)q * a.a_sl;
+        if (!F32) {
+          // bf16: issue every load of the row (o, dO, g, lse) before the first store — the
+          // stores may alias the inputs as far as the compiler knows, so it would not hoist them
+          constexpr int NV = DP / 8;
+          uint4 ov[NV], dv[NV], gv[NV];
+          const __nv_bfloat16* o_p = reinterpret_cast<const __nv_bfloat16*>(a.o) + orow;
+          const __nv_bfloat16* d_p = reinterpret_cast<const __nv_bfloat16*>(a.dout) + orow;
+          const __nv_bfloat16* g_p = reinterpret_cast<const __nv_bfloat16*>(a.g) + grow;
 #pragma unroll
-        for (int d0 = 0; d0 < DP; d0 += 8) {  // unrolled: every row load in flight at once
+          for (int x = 0; x < NV; ++x) {
+            ov[x] = dv[x] = gv[x] = make_uint4(0, 0, 0, 0);
+            if (x * 8 < a.D) {
+              ov[x] = __ldg(reinterpret_cast<const uint4*>(o_p + x * 8));
+              dv[x] = __ldg(reinterpret_cast<const uint4*>(d_p + x * 8));
+              if (a.g) gv[x] = __ldg(reinterpret_cast<const uint4*>(g_p + x * 8));
+            }
+          }
+          const float l = a.lse[(b * a.H + h) * a.Lq + q];
+#pragma unroll
+          for (int x = 0; x < NV; ++x) {
+            if (x * 8 >= a.D) break;
+            const uint32_t ou[4] = {ov[x].x, ov[x].y, ov[x].z, ov[x].w};
+            const uint32_t du[4] = {dv[x].x, dv[x].y, dv[x].z, dv[x].w};
+            const uint32_t gu[4] = {gv[x].x, gv[x].y, gv[x].z, gv[x].w};
+            uint32_t pa[4], pg[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float o0 = bf16_lo(ou[e]), o1 = bf16_hi(ou[e]);
+              const float d0v = bf16_lo(du[e]), d1v = bf16_hi(du[e]);
+              Dq = fmaf(d0v, o0, fmaf(d1v, o1, Dq));
+              if (a.g) {
+                const float s0 = 1.f / (1.f + __expf(-bf16_lo(gu[e])));
+                const float s1 = 1.f / (1.f + __expf(-bf16_hi(gu[e])));
+                pa[e] = pack_bf16(d0v * s0, d1v * s1);
+                pg[e] = pack_bf16(d0v * o0 * (1.f - s0), d1v * o1 * (1.f - s1));
+              }
+            }
+            if (a.g) {
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow + x * 8) =
+                  make_uint4(pa[0], pa[1], pa[2], pa[3]);
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dg) + grow + x * 8) =
+                  make_uint4(pg[0], pg[1], pg[2], pg[3]);
+            }
+          }
+          lv = sgn * (l == -INFINITY ? INFINITY : l * kLog2e);  // no kept key -> P = 0
+        } else {
+#pragma unroll
+        for (int d0 = 0; d0 < DP; d0 += 8) {  // fp32 verification path
           if (d0 >= a.D) break;
           float o8[8], do8[8], g8[8];
           if (F32) {
@@ -97,9 +143,6 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
             }
           }
         }
-        if (!F32) {
-          const float l = a.lse[(b * a.H + h) * a.Lq + q];
-          lv = sgn * (l == -INFINITY ? INFINITY : l * kLog2e);  // no kept key -> P = 0
         }
       }
       sD[hi][qi] = sgn * Dq;
