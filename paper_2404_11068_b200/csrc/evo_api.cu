@@ -532,6 +532,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dq = (__nv_bfloat16*)dq; fa.q_sb = d->q_str[0]; fa.q_sh = d->q_str[1]; fa.q_sl = d->q_str[2];
     fa.dq_acc = dqacc;
     fa.pairx = pairx ? 1 : 0;
+    static const int bwd_flags = getenv("EVO_BWD_FLAGS") ? atoi(getenv("EVO_BWD_FLAGS")) : 0;
+    fa.flags = bwd_flags;
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
     static const bool dbg_timing_b = getenv("EVO_DEBUG_TIMING") != nullptr;
     fa.dbg = dbg_timing_b ? evo::fwd_debug_ptr() : nullptr;

@@ -24,10 +24,14 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
   __shared__ float sD[kHC][32], sL[kHC][32];
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
   const int nqb = Lq_pad / 32;
-  const int64_t b = blockIdx.x / nqb;
-  const int q0 = (blockIdx.x % nqb) * 32;
   const bool hfast = a.o_sh < a.o_sl;
   const float sgn = a.negate ? -1.f : 1.f;
+  // persistent over (b, 32-query block) items: a short-lived block per item left the SMs half
+  // empty (one wave with a long ramp-down)
+  const int64_t nitems = (int64_t)a.B * nqb;
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  const int64_t b = item / nqb;
+  const int q0 = (int)(item % nqb) * 32;
   for (int h0 = 0; h0 < a.H; h0 += kHC) {
     const int hc = min(kHC, a.H - h0);
     for (int r = threadIdx.x; r < 32 * hc; r += blockDim.x) {
@@ -157,13 +161,14 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
     }
     __syncthreads();
   }
+  }
 }
 
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
-  const int64_t blocks = (int64_t)a.B * (Lq_pad / 32);
-  if (blocks == 0) return cudaSuccess;
-  const unsigned g = (unsigned)blocks;
+  const int64_t items = (int64_t)a.B * (Lq_pad / 32);
+  if (items == 0) return cudaSuccess;
+  const unsigned g = (unsigned)(items < 148 * 6 ? items : 148 * 6);
   if (f32) {
     if (a.D <= 16) bwd_pre_kernel<true, 16><<<g, 256, 0, st>>>(a);
     else if (a.D <= 32) bwd_pre_kernel<true, 32><<<g, 256, 0, st>>>(a);
@@ -714,7 +719,50 @@ __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
   }
 }
 
+// k-contiguous destination (the common case): a thread per 4 consecutive keys of a row, every
+// part's float4 in flight before the (fixed-order) sum, one float4 store
+__global__ void __launch_bounds__(256) dbias_reduce_k4_kernel(const ReduceArgs a) {
+  const int Lq_pad = ((a.Lq + 127) / 128) * 128, Lk_pad = ((a.Lk + 127) / 128) * 128;
+  const int64_t plane = (int64_t)a.H * Lq_pad * Lk_pad;
+  const int nk4 = (a.Lk + 3) / 4;
+  const int64_t n = a.nb * a.H * (int64_t)a.Lq * nk4;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx % nk4) * 4;
+    int64_t t = idx / nk4;
+    const int q = (int)(t % a.Lq);
+    t /= a.Lq;
+    const int h = (int)(t % a.H);
+    const int64_t bb = t / a.H;
+    const float4* src = reinterpret_cast<const float4*>(
+        a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < a.nparts; c0 += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        v[c] = c0 + c < a.nparts ? src[(int64_t)(c0 + c) * (plane / 4)] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) { acc.x += v[c].x; acc.y += v[c].y; acc.z += v[c].z; acc.w += v[c].w; }
+    }
+    float* dst = a.dbias + bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + k;
+    if (k + 3 < a.Lk && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+      *reinterpret_cast<float4*>(dst) = acc;
+    } else {
+      const float e4[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int e = 0; e < 4 && k + e < a.Lk; ++e) dst[e] = e4[e];
+    }
+  }
+}
+
 cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st) {
+  if (!a.q_fast && a.s_k == 1) {
+    const int64_t n = a.nb * a.H * (int64_t)a.Lq * ((a.Lk + 3) / 4);
+    if (n == 0) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    dbias_reduce_k4_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   const int64_t blocks = a.nb * a.H * (int64_t)((a.Lq + 31) / 32) * ((a.Lk + 31) / 32);
   if (blocks == 0) return cudaSuccess;
   dbias_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);

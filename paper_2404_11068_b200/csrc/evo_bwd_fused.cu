@@ -513,10 +513,15 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
       tc_fence_after();
       uint32_t rs[32], rd[32];
+      const int qcol = t * 128 + s * 32;  // first query of this sub-tile
+      // Σ_b dSᵀ so far for these 32 columns (this thread's own lane and columns, last written
+      // one batch row ago): loaded with Sᵀ/dPᵀ so one wait covers all three
+      uint32_t acc[32];
       {
         const uint32_t tS = tS0 + g * 64;
         tmem_ld32(tS + lane_base, rs);
         tmem_ld32(tS + 32 + lane_base, rd);
+        if (BIAS && bi > 0) tmem_ld32(tDB + lane_base + qcol, acc);
       }
       tmem_wait_ld();
       tc_fence_before();
@@ -524,7 +529,6 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) mbar_arrive(bar_sfree + 8 * g);
       mbar_wait(bar_in + 8 * st, (T >> 1) & 1);  // lse2 / D of this query tile visible
       const uint32_t vbase = s0 + C::oVec + st * 1024 + s * 32 * 4;
-      const int qcol = t * 128 + s * 32;  // first query of this sub-tile
       uint32_t pk[16], dk2[16];
       float ds[32];
 #pragma unroll
@@ -565,13 +569,10 @@ __global__ void __launch_bounds__(384, 1)
         for (int i = 0; i < 32; ++i) ds[i] = 0.f;
       }
       if (BIAS) {  // Σ_b dSᵀ in TMEM (this thread's lane, this sub-tile's 32 query columns)
-        uint32_t acc[32];
         if (bi == 0) {  // first batch row of the chunk initialises the (uninitialised) TMEM
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[i] = __float_as_uint(ds[i]);
         } else {
-          tmem_ld32(tDB + lane_base + qcol, acc);
-          tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const uint64_t s2 = f2_add(((uint64_t)acc[i + 1] << 32) | acc[i], f2_pack(ds[i], ds[i + 1]));

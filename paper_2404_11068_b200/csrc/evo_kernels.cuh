@@ -139,6 +139,7 @@ struct BwdFusedArgs {
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
   unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
   int pairx;  // two key tiles: CTA pair (cluster of 2) sums dQ over DSMEM, bf16 dq via TMA
+  int flags;  // experiment switches (EVO_BWD_FLAGS), 0 in production
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da;
