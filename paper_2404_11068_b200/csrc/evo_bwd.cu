@@ -769,26 +769,30 @@ cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// dq = bf16(scale · Σ_p part_p): 8 elements per thread, rows visited in the order of the smaller
-// of the (h, l) strides of dq (the parts use the same order, see ws_layout)
+// dq = bf16(scale · Σ_p part_p): 8 elements per thread (adjacent threads on adjacent 32-byte
+// chunks: coalesced), rows visited in the order of the smaller of the (h, l) strides of dq (the
+// parts use the same order, see ws_layout); 32-bit index math (rows < 2^31 checked by the launcher)
+template <int DP>
 __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
-  const int nd = a.D / 8;
-  const int64_t n8 = (int64_t)a.B * a.H * a.Lq * nd;
+  constexpr int ND = DP / 8;  // 8-element chunks per padded row
+  const int nd = (a.D + 7) / 8;
+  const uint32_t rows = (uint32_t)a.B * a.H * a.Lq;
+  const uint32_t n8 = rows * (uint32_t)nd;
   const bool hfast = a.q_sh < a.q_sl;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n8;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int d0 = (int)(idx % nd) * 8;
-    int64_t r = idx / nd;
-    int h, q;
-    if (hfast) { h = (int)(r % a.H); r /= a.H; q = (int)(r % a.Lq); r /= a.Lq; }
-    else { q = (int)(r % a.Lq); r /= a.Lq; h = (int)(r % a.H); r /= a.H; }
+  (void)ND;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n8; idx += gridDim.x * blockDim.x) {
+    const uint32_t d0 = (idx % (uint32_t)nd) * 8;
+    uint32_t r = idx / (uint32_t)nd;
+    uint32_t h, q;
+    if (hfast) { h = r % (uint32_t)a.H; r /= (uint32_t)a.H; q = r % (uint32_t)a.Lq; r /= (uint32_t)a.Lq; }
+    else { q = r % (uint32_t)a.Lq; r /= (uint32_t)a.Lq; h = r % (uint32_t)a.H; r /= (uint32_t)a.H; }
     const int64_t b = r;
-    const int64_t src = b * a.p_sb + h * a.p_sh + (int64_t)q * a.p_sl + d0;
-    float4 x = *reinterpret_cast<const float4*>(a.acc + src);
-    float4 y = *reinterpret_cast<const float4*>(a.acc + src + 4);
+    const float* src = a.acc + b * a.p_sb + (int64_t)h * a.p_sh + (int64_t)q * a.p_sl + d0;
+    float4 x = __ldg(reinterpret_cast<const float4*>(src));
+    float4 y = __ldg(reinterpret_cast<const float4*>(src) + 1);
     for (int p = 1; p < a.nparts; ++p) {
-      const float4 x2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + src);
-      const float4 y2 = *reinterpret_cast<const float4*>(a.acc + p * a.part_stride + src + 4);
+      const float4 x2 = __ldg(reinterpret_cast<const float4*>(src + p * a.part_stride));
+      const float4 y2 = __ldg(reinterpret_cast<const float4*>(src + p * a.part_stride) + 1);
       x.x += x2.x; x.y += x2.y; x.z += x2.z; x.w += x2.w;
       y.x += y2.x; y.y += y2.y; y.z += y2.z; y.w += y2.w;
     }
@@ -797,15 +801,19 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
     st.y = pack_bf16(x.z * a.scale, x.w * a.scale);
     st.z = pack_bf16(y.x * a.scale, y.y * a.scale);
     st.w = pack_bf16(y.z * a.scale, y.w * a.scale);
-    *reinterpret_cast<uint4*>(a.dq + b * a.q_sb + h * a.q_sh + (int64_t)q * a.q_sl + d0) = st;
+    *reinterpret_cast<uint4*>(a.dq + b * a.q_sb + (int64_t)h * a.q_sh + (int64_t)q * a.q_sl + d0) = st;
   }
 }
 
 cudaError_t launch_dq_convert(const ConvertArgs& a, cudaStream_t st) {
-  const int64_t n8 = (int64_t)a.B * a.H * a.Lq * (a.D / 8);
+  const int64_t n8 = (int64_t)a.B * a.H * a.Lq * ((a.D + 7) / 8);
   if (n8 == 0) return cudaSuccess;
+  if (n8 >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   const int64_t blocks = (n8 + 255) / 256;
-  dq_convert_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(a);
+  const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  if (a.D <= 16) dq_convert_kernel<16><<<g, 256, 0, st>>>(a);
+  else if (a.D <= 32) dq_convert_kernel<32><<<g, 256, 0, st>>>(a);
+  else dq_convert_kernel<64><<<g, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
