@@ -260,11 +260,8 @@ __global__ void __launch_bounds__(128, 4)
     const uint64_t negm2 = f2_pack(negm, negm);
     uint64_t ls[4] = {0, 0, 0, 0};
     uint32_t pk[32];
-    const int nexp = (a.flags & 32) ? 0 : 32;  // experiment: skip the exps (wrong results)
 #pragma unroll
-    for (int i = 0; i < 32; ++i) pk[i] = 0;
-#pragma unroll
-    for (int i = 0; i < nexp; ++i) {
+    for (int i = 0; i < 32; ++i) {
       float y0, y1;
       f2_unpack(f2_fma(f2_pack(x[2 * i], x[2 * i + 1]), log2e2, negm2), y0, y1);
       const float p0 = fast_exp2(y0), p1 = fast_exp2(y1);
