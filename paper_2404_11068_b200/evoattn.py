@@ -13,6 +13,7 @@ Tensor conventions (logical views; any strides, head dim unit-stride):
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import threading
 
@@ -59,6 +60,18 @@ class PairBiasDesc(ctypes.Structure):
     ]
 
 
+class GlobalAttnDesc(ctypes.Structure):
+    """Mirror of evo_global_attn_desc_t (include/evo_global_attn.h)."""
+    _fields_ = [
+        ("B", ctypes.c_int64), ("S", ctypes.c_int32), ("H", ctypes.c_int32),
+        ("D", ctypes.c_int32), ("scale", ctypes.c_float),
+        ("q_str", ctypes.c_int64 * 3), ("k_str", ctypes.c_int64 * 2),
+        ("v_str", ctypes.c_int64 * 2), ("g_str", ctypes.c_int64 * 3),
+        ("o_str", ctypes.c_int64 * 3), ("has_mask", ctypes.c_int32),
+        ("mask_str", ctypes.c_int64 * 2),
+    ]
+
+
 def lib_path() -> str:
     return _LIB_PATH
 
@@ -100,6 +113,11 @@ def load():
             lib.evo_pair_bias_bwd_workspace_bytes.restype = sz
             lib.evo_pair_bias_bwd.argtypes = [pdp] + [vp] * 12 + [sz, vp]
             lib.evo_pair_bias_bwd.restype = i32
+            gdp = ctypes.POINTER(GlobalAttnDesc)
+            lib.evo_global_attn_fwd.argtypes = [gdp] + [vp] * 9
+            lib.evo_global_attn_fwd.restype = i32
+            lib.evo_global_attn_bwd.argtypes = [gdp] + [vp] * 13
+            lib.evo_global_attn_bwd.restype = i32
             _lib = lib
     return _lib
 
@@ -312,3 +330,45 @@ def pair_bias_bwd(z, gamma, beta, W, mean, rstd, dbias, eps=1e-5, workspace=None
                                     _ptr(dz), _ptr(dgamma), _ptr(dbeta), _ptr(dW),
                                     _ptr(workspace), need, _stream(stream)))
     return {"dz": dz, "dgamma": dgamma, "dbeta": dbeta, "dW": dW}
+
+
+# ----------------------------------------------------------------------------- global column attention
+def _ga_desc(q, k, v, g, o, mask, scale):
+    d = GlobalAttnDesc()
+    d.B, d.S, d.H, d.D = q.shape
+    d.scale = float(scale if scale is not None else 1.0 / math.sqrt(q.shape[-1]))
+    d.q_str = (ctypes.c_int64 * 3)(*q.stride()[:3])
+    d.k_str = (ctypes.c_int64 * 2)(*k.stride()[:2])
+    d.v_str = (ctypes.c_int64 * 2)(*v.stride()[:2])
+    d.g_str = (ctypes.c_int64 * 3)(*g.stride()[:3])
+    d.o_str = (ctypes.c_int64 * 3)(*o.stride()[:3])
+    if mask is not None:
+        d.has_mask = 1
+        d.mask_str = (ctypes.c_int64 * 2)(*mask.stride())
+    return d
+
+
+def global_attn_fwd(q, k, v, g, mask=None, scale=None, stream=None):
+    """Extra-MSA global column attention core (include/evo_global_attn.h, AF2 Alg. 19 l.3/5/6).
+    q, g [B, S, H, D]; k, v [B, S, D] (one shared head); mask [B, S].  Returns (o, lse, qbar)."""
+    o = torch.empty_like(q)
+    B, S, H, D = q.shape
+    lse = torch.empty((B, H), dtype=torch.float32, device=q.device)
+    qbar = torch.empty((B, H, D), dtype=torch.float32, device=q.device)
+    d = _ga_desc(q, k, v, g, o, mask, scale)
+    m = mask.view(torch.uint8) if (mask is not None and mask.dtype == torch.bool) else mask
+    _check(load().evo_global_attn_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(g),
+                                      _ptr(o), _ptr(lse), _ptr(qbar), _stream(stream)))
+    return o, lse, qbar
+
+
+def global_attn_bwd(q, k, v, g, lse, qbar, dout, mask=None, scale=None, stream=None):
+    """Backward of global_attn_fwd.  Returns dict dq, dk, dv, dg (the inputs' strides)."""
+    o_like = dout if dout.stride() == q.stride() else dout.contiguous()
+    d = _ga_desc(q, k, v, g, o_like, mask, scale)
+    dq, dk, dv, dg = _alloc_like(q), _alloc_like(k), _alloc_like(v), _alloc_like(g)
+    m = mask.view(torch.uint8) if (mask is not None and mask.dtype == torch.bool) else mask
+    _check(load().evo_global_attn_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(g),
+                                      _ptr(lse), _ptr(qbar), _ptr(o_like), _ptr(dq), _ptr(dk),
+                                      _ptr(dv), _ptr(dg), _stream(stream)))
+    return {"dq": dq, "dk": dk, "dv": dv, "dg": dg}

@@ -60,6 +60,23 @@ def test_pair_bias_exports_and_descriptor(lib, tmp_path):
         assert int(out[f]) == getattr(PairBiasDesc, f).offset, f
 
 
+def test_global_attn_exports_and_descriptor(lib, tmp_path):
+    for n in _declared("evo_global_attn.h"):
+        assert hasattr(lib, n), f"libevoattn.so does not export {n}"
+    from paper_2404_11068_b200.evoattn import GlobalAttnDesc
+    fields = [f[0] for f in GlobalAttnDesc._fields_]
+    src = tmp_path / "ga.c"
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof(evo_global_attn_desc_t, {f}));' for f in fields)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "evo_global_attn.h"\n'
+                   'int main(void){printf("size %zu\\n", sizeof(evo_global_attn_desc_t));' + body + "}")
+    exe = tmp_path / "ga"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    assert int(out["size"]) == ctypes.sizeof(GlobalAttnDesc)
+    for f in fields:
+        assert int(out[f]) == getattr(GlobalAttnDesc, f).offset, f
+
+
 def test_pair_bias_validation(lib):
     from paper_2404_11068_b200.evoattn import PairBiasDesc
     d = PairBiasDesc()

@@ -32,6 +32,7 @@ CASES = [
     (2, 1, 384, 32, "shared", False, True, "prefix", False, "blhd"),     # cfg5-like L
     (2, 2, 520, 8, None, False, True, "prefix", True, "lbhd"),           # extra-MSA-like, 5 tiles
     (2, 1, 384, 32, None, False, True, "prefix_fm", False, "blhd"),      # no bias, 3 key tiles
+    (6, 8, 256, 8, "shared", False, True, "prefix", False, "blhd"),      # extra-MSA row (f3) 8x8
 ]
 
 

@@ -14,6 +14,7 @@ CFG = [  # name, B, H, L, D, bias, storage ("bl": [B,L,H,D], "lb": [L,B,H,D]), b
     ("cfg3 tri-end 256", 256, 4, 256, 32, True, "lb", True),
     ("block MSA col 256x128", 256, 8, 128, 32, False, "lb", False),
     ("cfg4 extra-MSA col 1024, 8x8", 256, 8, 1024, 8, False, "lb", False),
+    ("f3 extra-MSA row 1024x256, 8x8", 1024, 8, 256, 8, True, "bl", False),
     ("cfg5 row 512x384", 512, 8, 384, 32, True, "bl", False),
     ("cfg5 col 384x512", 384, 8, 512, 32, False, "lb", False),
     ("cfg5 tri-start 384", 384, 4, 384, 32, True, "bl", False),
@@ -58,3 +59,18 @@ for name, B, H, L, D, bias, st, bt in CFG:
                 "bwd_us": round(tb, 1), "fwd_bwd_us": round(tfb, 1),
                 "tflops_alg": round(fl / (tfb * 1e-6) / 1e12, 1)})
     print(json.dumps(res[-1]), flush=True)
+
+# f3: extra-MSA global column attention core (AF2 Alg. 19) at N_extra=1024, N_res=256, 8x8
+B, S, H, D = 256, 1024, 8, 8
+gq = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+gg = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+gk = torch.randn((S, B, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+gv = torch.randn((S, B, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+gm = torch.ones((S, B), dtype=torch.uint8, device=dev).t()
+o, lse, qbar = evoattn.global_attn_fwd(gq, gk, gv, gg, gm)
+tf = timed(lambda: evoattn.global_attn_fwd(gq, gk, gv, gg, gm))
+tb = timed(lambda: evoattn.global_attn_bwd(gq, gk, gv, gg, lse, qbar, o, gm))
+by_f = (2 * B * S * H * D + 2 * B * S * D) * 2 + B * S * H * D * 2
+by_b = (3 * B * S * H * D + 2 * B * S * D) * 2 + (2 * B * S * H * D + 2 * B * S * D) * 2
+print(json.dumps({"config": "f3 extra-MSA global column attention 256x1024, 8x8", "fwd_us": round(tf, 1),
+                  "bwd_us": round(tb, 1), "fwd_GBps": round(by_f / tf / 1e3), "bwd_GBps": round(by_b / tb / 1e3)}))
