@@ -74,6 +74,61 @@ def kernel_alg(name, B, H, L, D, bias):
     return 0.0, 0.0, 0.0
 
 
+def kernel_roofline(per, modules, clk):
+    """Per-kernel table and the dominant kernel's roofline object from per-launch device times
+    (ms, lists keyed by the C ABI trace label) and the calls' shapes [(name, B, H, L, bias)]:
+    achieved = algorithmic work per launch (kernel_alg, averaged over the modules) ÷ the mean
+    launch time; peak = MEASURED_PEAKS.json; MUFU peak = 148 SMs x 16 ex2/clk x the SM clock
+    sampled under load."""
+    calls = []
+    for name, B, H, L, bias in modules:
+        calls.append(("fwd_bf16", B, H, L, bias))
+        calls += [("bwd_pre", B, H, L, bias), ("bwd_fused", B, H, L, bias)]
+        if L > 128:
+            calls.append(("dq_convert", B, H, L, bias))
+        if bias:
+            calls.append(("dbias_reduce", B, H, L, bias))
+    work = {}
+    for kname, B, H, L, bias in calls:
+        f, by, ex = kernel_alg(kname, B, H, L, C_HEAD, bias)
+        w = work.setdefault(kname, [0.0, 0.0, 0.0, 0])
+        w[0] += f; w[1] += by; w[2] += ex; w[3] += 1
+    tot_traced = sum(sum(v) for v in per.values())
+    kernels = {}
+    for k, v in per.items():
+        n = len(v)
+        w = work.get(k, [0, 0, 0, 1])
+        per_launch_ms = sum(v) / n
+        f, by, ex = w[0] / w[3], w[1] / w[3], w[2] / w[3]
+        kernels[k] = {"launches": n, "ms_per_launch": per_launch_ms,
+                      "share": sum(v) / tot_traced,
+                      "tflops": f / (per_launch_ms * 1e-3) / 1e12,
+                      "gbs": by / (per_launch_ms * 1e-3) / 1e9,
+                      "gexps": ex / (per_launch_ms * 1e-3) / 1e9}
+    dom = max(kernels, key=lambda k: kernels[k]["share"])
+    pk = measured_peaks()
+    sm_mhz = (clk or {}).get("sm_mhz") or pk["sm_max_mhz"]
+    mufu_peak = 148 * 16 * sm_mhz * 1e6 / 1e9  # Gex2/s (16 ex2/clk/SM, DESIGN.md §5)
+    dk = kernels[dom]
+    fr_t = dk["tflops"] / pk["bf16_tflops"]
+    fr_h = dk["gbs"] / pk["hbm_gbs"]
+    fr_x = dk["gexps"] / mufu_peak
+    if fr_x >= max(fr_t, fr_h):
+        roof = {"bound": "alu", "achieved": dk["gexps"], "peak": mufu_peak, "unit": "Gexp2/s",
+                "frac": fr_x}
+    elif fr_h >= fr_t:
+        roof = {"bound": "hbm", "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": fr_h}
+    else:
+        roof = {"bound": "tensor", "achieved": dk["tflops"], "peak": pk["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": fr_t}
+    roof.update({"kernel": dom, "traffic": load_traffic(dom), "peak_source": pk["source"],
+                 "fracs": {"tensor": fr_t, "hbm": fr_h, "mufu": fr_x},
+                 "mufu_peak_note": f"148 SM x 16 ex2/clk x {sm_mhz:.0f} MHz (median SM clock "
+                                   "under load)"})
+    return kernels, roof
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
@@ -338,53 +393,7 @@ def run_gpu(args):
     per = {}
     for i, lab in enumerate(labels):
         per.setdefault(lab, []).append(trace_ev[2 * i].elapsed_time(trace_ev[2 * i + 1]))
-    # algorithmic work per launch, per kernel kind, averaged over the four modules
-    calls = []
-    for name, B, H, L, bias in MODULES:
-        calls.append(("fwd_bf16", B, H, L, bias))
-        calls += [("bwd_pre", B, H, L, bias), ("bwd_fused", B, H, L, bias)]
-        if L > 128:
-            calls.append(("dq_convert", B, H, L, bias))
-        if bias:
-            calls.append(("dbias_reduce", B, H, L, bias))
-    work = {}
-    for kname, B, H, L, bias in calls:
-        f, by, ex = kernel_alg(kname, B, H, L, C_HEAD, bias)
-        w = work.setdefault(kname, [0.0, 0.0, 0.0, 0])
-        w[0] += f; w[1] += by; w[2] += ex; w[3] += 1
-    tot_traced = sum(sum(v) for v in per.values())
-    kernels = {}
-    for k, v in per.items():
-        n = len(v)
-        w = work.get(k, [0, 0, 0, 1])
-        per_launch_ms = sum(v) / n
-        f, by, ex = w[0] / w[3], w[1] / w[3], w[2] / w[3]
-        kernels[k] = {"launches": n, "ms_per_launch": per_launch_ms,
-                      "share": sum(v) / tot_traced,
-                      "tflops": f / (per_launch_ms * 1e-3) / 1e12,
-                      "gbs": by / (per_launch_ms * 1e-3) / 1e9,
-                      "gexps": ex / (per_launch_ms * 1e-3) / 1e9}
-    dom = max(kernels, key=lambda k: kernels[k]["share"])
-    pk = measured_peaks()
-    sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
-    mufu_peak = 148 * 16 * sm_mhz * 1e6 / 1e9  # Gex2/s (16 ex2/clk/SM)
-    dk = kernels[dom]
-    fr_t = dk["tflops"] / pk["bf16_tflops"]
-    fr_h = dk["gbs"] / pk["hbm_gbs"]
-    fr_x = dk["gexps"] / mufu_peak
-    if fr_x >= max(fr_t, fr_h):
-        roof = {"bound": "alu", "achieved": dk["gexps"], "peak": mufu_peak, "unit": "Gexp2/s",
-                "frac": fr_x}
-    elif fr_h >= fr_t:
-        roof = {"bound": "hbm", "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": fr_h}
-    else:
-        roof = {"bound": "tensor", "achieved": dk["tflops"], "peak": pk["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": fr_t}
-    roof.update({"kernel": dom, "traffic": load_traffic(dom), "peak_source": pk["source"],
-                 "fracs": {"tensor": fr_t, "hbm": fr_h, "mufu": fr_x},
-                 "mufu_peak_note": f"148 SM x 16 ex2/clk x {sm_mhz:.0f} MHz (median SM clock "
-                                   "under load)"})
+    kernels, roof = kernel_roofline(per, [(n, B, H, L, bias) for n, B, H, L, bias in MODULES], clk)
 
     # e2e: host buffers through the same C ABI, h2d + d2h inside the timed region
     e2e = run_e2e(torch, evoattn, mods, args, dev, stream, flops)
@@ -402,7 +411,7 @@ def run_gpu(args):
                    else "warm", "parallelism": "single GPU",
                    "launch": "CUDA graph of the step" if graph is not None else "eager",
                    "kernel_timing": "per-launch CUDA events over K further eager steps"},
-        "pct_of_peak": {"tensor_measured": value / pk["bf16_tflops"],
+        "pct_of_peak": {"tensor_measured": value / measured_peaks()["bf16_tflops"],
                         "tensor_nominal": value / 2250.0},
         "roofline": roof,
         "kernels": kernels,

@@ -97,12 +97,32 @@ def run(args, metric):
     flops = dap.block_flops(n_seq, n_res)
     # our kernels in the timed region: the attention core's launches (C ABI count) + one
     # pack/unpack per transpose when N > 1 (NCCL's own kernels are library code, not counted)
-    if graph is not None:  # replays do not pass through the binding: count one eager step
-        attn.launches = 0
+    # per-kernel device time from K eager steps with each attention launch bracketed by CUDA
+    # events (graph replays cannot be timed per kernel); also the launch count of our kernels
+    import ctypes
+    from bench import kernel_roofline
+    lib = evoattn.load()
+    trace_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * 64 * args.steps)]
+    for e in trace_ev:
+        e.record(stream)
+    torch.cuda.synchronize()
+    arr = (ctypes.c_void_p * len(trace_ev))(*[e.cuda_event for e in trace_ev])
+    lib.evo_trace_enable(arr, len(trace_ev))
+    attn.launches = 0
+    for _ in range(args.steps):
         step()
-        torch.cuda.synchronize()
-        attn.launches *= args.steps
+    torch.cuda.synchronize()
+    ntr = lib.evo_trace_count()
+    labels = [lib.evo_trace_label(i).decode() for i in range(ntr)]
+    lib.evo_trace_enable(None, 0)
+    per = {}
+    for i, lab in enumerate(labels):
+        per.setdefault(lab, []).append(trace_ev[2 * i].elapsed_time(trace_ev[2 * i + 1]))
+    pl = dap.plan(world, n_seq, n_res)
+    mods = [("row", *pl["row"], True), ("col", *pl["col"], False), ("start", *pl["start"], True),
+            ("end", *pl["end"], True)]
     launches = attn.launches + (8 * args.steps if world > 1 else 0)
+    kernels, roof = kernel_roofline(per, mods, clk)
     e2e = _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops)
     if rank == 0:
         line = {
@@ -117,6 +137,8 @@ def run(args, metric):
                        "collectives_per_block": {"a2a": 8, "allgather": 3, "reduce_scatter": 3},
                        "launch": "CUDA graph of the step" if graph is not None else "eager"},
             "clocks": clk,
+            "roofline": roof,
+            "kernels": kernels,
             "e2e": e2e,
             "gpu_launches": launches,
         }
