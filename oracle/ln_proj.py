@@ -1,0 +1,28 @@
+"""fp64 oracle of the LayerNorm + batched q/k/v/g projection (PAPER.md
+L273 "fused LayerNorm, MHA and its previous four GEMMs", L296-297 "GEMM Batching: four linear
+layers have no dependency on each other"; SPEC.md L174-182 qkvg_project; AF2 Alg. 7 l.1-4).
+
+TEST INFRASTRUCTURE ONLY (same rule as oracle/evo_oracle.c).
+
+  y = LayerNorm(x)·γ + β               (two-pass mean / biased variance, fp64)
+  [q | k | v | g_logits] = y · [W_q | W_k | W_v | W_g] + [0 | 0 | 0 | b_g]
+The four projections are computed as four separate products (the definition), so the pin
+"equal to four separate GEMMs" is checked against the fused kernel, not assumed.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def ln_qkvg_fwd(x, gamma, beta, W, bias_g=None, eps=1e-5):
+    """x [rows, C]; gamma, beta [C]; W [C, 4, N1] (q, k, v, g blocks of width N1 = H·D);
+    bias_g [N1] or None.  Returns Y [rows, 4, N1] (q, k, v, gate logits)."""
+    x = np.asarray(x, np.float64)
+    mean = x.mean(axis=1, keepdims=True)
+    var = ((x - mean) ** 2).mean(axis=1, keepdims=True)
+    y = (x - mean) / np.sqrt(var + eps) * np.asarray(gamma, np.float64) + np.asarray(beta, np.float64)
+    W = np.asarray(W, np.float64)
+    out = np.stack([y @ W[:, j, :] for j in range(4)], axis=1)
+    if bias_g is not None:
+        out[:, 3, :] += np.asarray(bias_g, np.float64)
+    return out
