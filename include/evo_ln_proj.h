@@ -1,0 +1,54 @@
+/*
+ * evo_ln_proj.h — C ABI of the fused LayerNorm + batched input projection that feeds the
+ * attention core: the "previous four GEMMs" of PAPER.md L273 and the GEMM batching of PAPER.md
+ * L296-297 ("Four linear layers have no dependency on each other. We bundled these linear layers
+ * into batch operations"); SPEC.md L174-182 qkvg_project.
+ *
+ *   for every row r:   μ_r = Σ_c x[r,c] / C,   σ²_r = Σ_c (x[r,c] − μ_r)² / C     (fp32)
+ *                      y[r,c] = bf16( (x[r,c] − μ_r)·rstd_r·γ_c + β_c ),  rstd_r = 1/sqrt(σ²_r + eps)
+ *                      out[r,n] = bf16( Σ_c y[r,c]·W[n,c] + b[n] )                  (fp32 accumulate)
+ *
+ * W is the four projection weights stacked along the output axis, in the nn.Linear [out, in]
+ * layout: rows [0, H·D) = W_q, then W_k, W_v, W_g (any stacking — the kernel sees one [N, C]
+ * matrix, so the MSA-global q/k/v/g of Alg. 19 with single-head k, v also fits).  b is an
+ * optional fp32 [N] vector (AF2: zeros for q, k, v and the gate bias for g; NULL = no bias).
+ * `out` row r holds the N projections contiguously, so each of q, k, v, g is a strided view
+ * [rows, H, D] that evo_attn_fwd takes directly (row stride out_ld, head stride D).
+ *
+ * Layouts: x [rows][C] bf16, row stride x_ld elements (multiple of 8, c unit-stride); W [N][C]
+ * bf16 dense; out [rows][N] bf16, row stride out_ld (>= N, multiple of 8); γ, β [C] fp32;
+ * mean, rstd [rows] fp32 (written when non-NULL, for a LayerNorm backward).
+ *
+ * Supported: C in {64, 128, 256}, N a multiple of 64 (<= 4096), rows >= 0, eps > 0.  Device
+ * pointers, 16-byte-aligned tensors, asynchronous on `stream`, errors returned (EVO_E_*), details
+ * in evo_last_error_detail(), no allocation (conventions of evo_attn.h).
+ */
+#ifndef EVO_LN_PROJ_H
+#define EVO_LN_PROJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "evo_attn.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int64_t rows;     /* M: rows of x / out                                          */
+  int32_t C;        /* input channels: 64, 128 or 256                               */
+  int32_t N;        /* stacked output features (4·H·D for q|k|v|g), multiple of 64  */
+  float eps;        /* LayerNorm epsilon, > 0 (AF2: 1e-5)                           */
+  int64_t x_ld;     /* row stride of x, elements                                    */
+  int64_t out_ld;   /* row stride of out, elements                                  */
+} evo_ln_proj_desc_t;
+
+evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void* x, const float* gamma,
+                             const float* beta, const void* W, const float* b, void* out,
+                             float* mean, float* rstd, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVO_LN_PROJ_H */

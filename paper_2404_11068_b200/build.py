@@ -21,7 +21,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 ATTN_SRCS = ["evo_api.cu", "evo_fwd.cu", "evo_fwd_ws.cu", "evo_fwd_occ.cu", "evo_fwd_pp.cu", "evo_bwd.cu",
              "evo_bwd_fused.cu", "evo_f32.cu", "evo_pair_bias.cu",
-             "evo_global_attn.cu"]
+             "evo_global_attn.cu", "evo_ln_proj.cu"]
 LIB_ATTN = os.path.join(HERE, "libevoattn.so")
 LIB_DAP = os.path.join(HERE, "libevodap.so")
 

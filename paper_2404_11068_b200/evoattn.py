@@ -72,6 +72,14 @@ class GlobalAttnDesc(ctypes.Structure):
     ]
 
 
+class LnProjDesc(ctypes.Structure):
+    """Mirror of evo_ln_proj_desc_t (include/evo_ln_proj.h)."""
+    _fields_ = [
+        ("rows", ctypes.c_int64), ("C", ctypes.c_int32), ("N", ctypes.c_int32),
+        ("eps", ctypes.c_float), ("x_ld", ctypes.c_int64), ("out_ld", ctypes.c_int64),
+    ]
+
+
 def lib_path() -> str:
     return _LIB_PATH
 
@@ -118,6 +126,8 @@ def load():
             lib.evo_global_attn_fwd.restype = i32
             lib.evo_global_attn_bwd.argtypes = [gdp] + [vp] * 13
             lib.evo_global_attn_bwd.restype = i32
+            lib.evo_ln_proj_fwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 9
+            lib.evo_ln_proj_fwd.restype = i32
             _lib = lib
     return _lib
 
@@ -372,3 +382,22 @@ def global_attn_bwd(q, k, v, g, lse, qbar, dout, mask=None, scale=None, stream=N
                                       _ptr(lse), _ptr(qbar), _ptr(o_like), _ptr(dq), _ptr(dk),
                                       _ptr(dv), _ptr(dg), _stream(stream)))
     return {"dq": dq, "dk": dk, "dv": dv, "dg": dg}
+
+
+def ln_proj_fwd(x, gamma, beta, W, b=None, eps=1e-5, out=None, stream=None):
+    """Fused LayerNorm + stacked projection (include/evo_ln_proj.h).
+    x [rows, C] bf16 (row stride x.stride(0)); W [N, C] bf16 (nn.Linear layout, q|k|v|g stacked);
+    gamma, beta [C] fp32; b [N] fp32 or None.  Returns (out [rows, N] bf16, mean, rstd)."""
+    rows, C = x.shape
+    N = W.shape[0]
+    if out is None:
+        out = torch.empty((rows, N), dtype=torch.bfloat16, device=x.device)
+    mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    d = LnProjDesc()
+    d.rows, d.C, d.N, d.eps = rows, C, N, eps
+    d.x_ld, d.out_ld = x.stride(0), out.stride(0)
+    _check(load().evo_ln_proj_fwd(ctypes.byref(d), _ptr(x), _ptr(gamma), _ptr(beta),
+                                  _ptr(W.contiguous()), _ptr(b), _ptr(out), _ptr(mean),
+                                  _ptr(rstd), _stream(stream)))
+    return out, mean, rstd

@@ -77,6 +77,36 @@ def test_global_attn_exports_and_descriptor(lib, tmp_path):
         assert int(out[f]) == getattr(GlobalAttnDesc, f).offset, f
 
 
+def test_ln_proj_exports_and_descriptor(lib, tmp_path):
+    for n in _declared("evo_ln_proj.h"):
+        assert hasattr(lib, n), f"libevoattn.so does not export {n}"
+    from paper_2404_11068_b200.evoattn import LnProjDesc
+    fields = [f[0] for f in LnProjDesc._fields_]
+    src = tmp_path / "lp.c"
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof(evo_ln_proj_desc_t, {f}));' for f in fields)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "evo_ln_proj.h"\n'
+                   'int main(void){printf("size %zu\\n", sizeof(evo_ln_proj_desc_t));' + body + "}")
+    exe = tmp_path / "lp"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    assert int(out["size"]) == ctypes.sizeof(LnProjDesc)
+    for f in fields:
+        assert int(out[f]) == getattr(LnProjDesc, f).offset, f
+
+
+def test_ln_proj_validation(lib):
+    from paper_2404_11068_b200.evoattn import LnProjDesc
+    d = LnProjDesc()
+    d.rows, d.C, d.N, d.eps, d.x_ld, d.out_ld = 256, 96, 512, 1e-5, 96, 512
+    p = ctypes.c_void_p(16)
+    lib.evo_ln_proj_fwd.restype = ctypes.c_int
+    assert lib.evo_ln_proj_fwd(ctypes.byref(d), p, p, p, p, None, p, None, None, None) == 4
+    d.C, d.N = 128, 100
+    assert lib.evo_ln_proj_fwd(ctypes.byref(d), p, p, p, p, None, p, None, None, None) == 4
+    d.N, d.x_ld = 512, 132
+    assert lib.evo_ln_proj_fwd(ctypes.byref(d), p, p, p, p, None, p, None, None, None) == 3
+
+
 def test_pair_bias_validation(lib):
     from paper_2404_11068_b200.evoattn import PairBiasDesc
     d = PairBiasDesc()
