@@ -19,7 +19,7 @@
  * bf16 dense; out [rows][N] bf16, row stride out_ld (>= N, multiple of 8); γ, β [C] fp32;
  * mean, rstd [rows] fp32 (written when non-NULL, for a LayerNorm backward).
  *
- * Supported: C in {64, 128, 256}, N a multiple of 64 (<= 4096), rows >= 0, eps > 0.  Device
+ * Supported: C in {64, 128, 256}, N a multiple of 64 (<= 2048), rows >= 0, eps > 0.  Device
  * pointers, 16-byte-aligned tensors, asynchronous on `stream`, errors returned (EVO_E_*), details
  * in evo_last_error_detail(), no allocation (conventions of evo_attn.h).
  */

@@ -1,11 +1,16 @@
 """Time evo_ln_proj_fwd (f2) at the AF2 module shapes; prints µs, GB/s and TFLOP/s per shape."""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch
 
 from paper_2404_11068_b200 import evoattn
 
 dev = torch.device("cuda:0")
+only = sys.argv[1] if len(sys.argv) > 1 else None
 for name, rows, C, N in [("msa_row/col", 128 * 256, 256, 1024), ("triangle", 256 * 256, 128, 512),
                          ("extra_msa", 1024 * 256, 64, 256)]:
+    if only and name != only:
+        continue
     x = torch.randn((rows, C), device=dev).to(torch.bfloat16)
     g, bt = torch.ones(C, device=dev), torch.zeros(C, device=dev)
     W = (torch.randn((N, C), device=dev) / C ** 0.5).to(torch.bfloat16)
