@@ -229,6 +229,33 @@ inline void trace_end(cudaStream_t st) {
   }
   ++t.n;
 }
+// Per-host-thread side stream (+ fork/join events) of the current device: the two independent
+// tails of the fused backward (dq parts -> bf16, dbias partials -> dbias) run concurrently, the
+// dbias reduce forked off the caller's stream and joined back before the call returns (so the
+// call stays stream-ordered; fork/join by events is also what CUDA-graph capture records).
+struct SideStream {
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+  thread_local SideStream ss;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (ss.dev != dev) {
+    SideStream n;
+    n.dev = dev;
+    if (cudaStreamCreateWithFlags(&n.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;  // callers fall back to running both tails on the caller's stream
+    }
+    ss = n;  // (a previous device's stream/events are left to the process teardown)
+  }
+  return &ss;
+}
+
 // launch wrapper: bracket one kernel launch with trace events
 template <class F>
 inline cudaError_t traced(cudaStream_t st, const char* label, F&& f) {
@@ -539,6 +566,23 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dbg = dbg_timing_b ? evo::fwd_debug_ptr() : nullptr;
     if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
     ++nl;
+    // fork: the dbias reduce runs on the side stream while dq_convert runs on the caller's
+    SideStream* ss = (dqacc && bm) ? side_stream() : nullptr;
+    cudaStream_t rst = st;
+    if (ss && cudaEventRecord(ss->fork, st) == cudaSuccess &&
+        cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess)
+      rst = ss->s;
+    else
+      (void)cudaGetLastError();
+    if (bm) {
+      evo::ReduceArgs ra{};
+      ra.nparts = fa.nchunks; ra.H = d->H; ra.Lq = d->Lq; ra.Lk = d->Lk; ra.nb = 1;
+      ra.partial = fa.partial; ra.dbias = dbias;
+      ra.s_b = 0; ra.s_h = d->bias_str[1]; ra.s_q = d->bias_str[2]; ra.s_k = d->bias_str[3];
+      ra.q_fast = bm == 2;
+      if ((e = traced(rst, "dbias_reduce", [&] { return evo::launch_dbias_reduce(ra, rst); })) != cudaSuccess) return cuda_fail(e, "dbias_reduce");
+      ++nl;
+    }
     if (dqacc) {
       evo::ConvertArgs ca{};
       ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
@@ -548,14 +592,10 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
       if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");
       ++nl;
     }
-    if (bm) {
-      evo::ReduceArgs ra{};
-      ra.nparts = fa.nchunks; ra.H = d->H; ra.Lq = d->Lq; ra.Lk = d->Lk; ra.nb = 1;
-      ra.partial = fa.partial; ra.dbias = dbias;
-      ra.s_b = 0; ra.s_h = d->bias_str[1]; ra.s_q = d->bias_str[2]; ra.s_k = d->bias_str[3];
-      ra.q_fast = bm == 2;
-      if ((e = traced(st, "dbias_reduce", [&] { return evo::launch_dbias_reduce(ra, st); })) != cudaSuccess) return cuda_fail(e, "dbias_reduce");
-      ++nl;
+    if (rst != st) {  // join
+      if ((e = cudaEventRecord(ss->join, rst)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(st, ss->join, 0)) != cudaSuccess)
+        return cuda_fail(e, "side-stream join");
     }
     g_launches = nl;
     return EVO_OK;
