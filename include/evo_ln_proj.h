@@ -48,6 +48,14 @@ evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void* x, const f
                              const float* beta, const void* W, const float* b, void* out,
                              float* mean, float* rstd, void* stream);
 
+/* The same kernel without the LayerNorm: out[r,n] = bf16( Σ_c x[r,c]·W[n,c] + b[n] ) — the
+ * attention module's output projection (SURVEY.md §8(f) f2 "and the output projection";
+ * [ext] AF2 Alg. 7 l.7 / Alg. 13 l.7, cited at PAPER.md L178), e.g. x = the gated attention
+ * output [rows, H·D] and W = W_o [c, H·D].  Same layouts, limits and conventions as above; eps,
+ * gamma, beta, mean and rstd do not apply. */
+evo_status_t evo_linear_fwd(const evo_ln_proj_desc_t* d, const void* x, const void* W,
+                            const float* b, void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

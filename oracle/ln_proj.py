@@ -26,3 +26,12 @@ def ln_qkvg_fwd(x, gamma, beta, W, bias_g=None, eps=1e-5):
     if bias_g is not None:
         out[:, 3, :] += np.asarray(bias_g, np.float64)
     return out
+
+
+def linear_fwd(x, W, b=None):
+    """out[r, n] = Σ_c x[r, c]·W[n, c] + b[n] (the output projection, [ext] AF2 Alg. 7 l.7);
+    W in the nn.Linear [out, in] layout.  The definition, in fp64."""
+    out = np.asarray(x, np.float64) @ np.asarray(W, np.float64).T
+    if b is not None:
+        out = out + np.asarray(b, np.float64)
+    return out

@@ -61,6 +61,7 @@ constexpr int kMaxN = 2048;              // bias staged in smem
 struct LnProjArgs {
   int64_t M;
   int N, NT, n_row_tiles, n_pairs;
+  int ln;  // 1: LayerNorm the x tile first (evo_ln_proj_fwd); 0: plain linear (evo_linear_fwd)
   float eps;
   const float *gamma, *beta, *b;
   float *mean, *rstd;
@@ -163,7 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   {  // per-CTA parameter staging: every lane of a warp then reads the same word (broadcast)
     float* gb = reinterpret_cast<float*>(smem_raw + (sGB - smem_u32(smem_raw)));
     for (int k = threadIdx.x; k < 2 * C + a.N; k += kThreads)
-      gb[k] = k < C ? a.gamma[k] : (k < 2 * C ? a.beta[k - C] : (a.b ? a.b[k - 2 * C] : 0.f));
+      gb[k] = k < 2 * C ? (a.ln ? (k < C ? a.gamma[k] : a.beta[k - C]) : 0.f)
+                        : (a.b ? a.b[k - 2 * C] : 0.f);
   }
   tc_fence_before();
   cluster_sync_all();  // barriers of both CTAs initialised before any multicast lands
@@ -244,6 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = i & 1, tile = 2 * p + rank;
       mbar_wait(xfull + 8 * b, (i >> 1) & 1);
       if (warp == 8 && lane == 0 && i < 4) LP_STAMP(1 + i);
+      if (!a.ln) {  // plain linear: the x tile is the A operand as loaded
+        mbar_arrive(yready + 8 * b);
+        continue;
+      }
 #pragma unroll 1
       for (int rg = 0; rg < 2; ++rg) {
         const uint32_t t = (warp - 8) * 16 + rg * 8 + r8;  // tile row
@@ -411,10 +417,9 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 }  // namespace
 }  // namespace evo
 
-extern "C" evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void* x,
-                                        const float* gamma, const float* beta, const void* W,
-                                        const float* b, void* out, float* mean, float* rstd,
-                                        void* stream) {
+static evo_status_t ln_proj_launch(const evo_ln_proj_desc_t* d, const void* x, const float* gamma,
+                                   const float* beta, const void* W, const float* b, void* out,
+                                   float* mean, float* rstd, void* stream, int ln) {
   using namespace evo;
   if (!d) return lp_fail(EVO_E_INVALID, "desc is NULL");
   if (d->rows < 0) return lp_fail(EVO_E_SHAPE, "rows = %lld < 0", (long long)d->rows);
@@ -423,16 +428,17 @@ extern "C" evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void*
   if (d->N <= 0 || d->N % 64 != 0 || d->N > kMaxN)
     return lp_fail(EVO_E_UNSUPPORTED, "N = %d must be a positive multiple of 64, <= %d", d->N,
                    kMaxN);
-  if (!(d->eps > 0.f)) return lp_fail(EVO_E_INVALID, "eps must be > 0");
+  if (ln && !(d->eps > 0.f)) return lp_fail(EVO_E_INVALID, "eps must be > 0");
   if (d->x_ld < d->C || d->x_ld % 8 != 0)
     return lp_fail(EVO_E_ALIGN, "x_ld = %lld must be >= C and a multiple of 8", (long long)d->x_ld);
   if (d->out_ld < d->N || d->out_ld % 8 != 0)
     return lp_fail(EVO_E_ALIGN, "out_ld = %lld must be >= N and a multiple of 8",
                    (long long)d->out_ld);
   if (d->rows == 0) return EVO_OK;
-  if (!x || !gamma || !beta || !W || !out)
-    return lp_fail(EVO_E_INVALID, "x, gamma, beta, W and out are required");
-  if (!al16(x) || !al16(W) || !al16(out) || !al16(gamma) || !al16(beta) || (b && !al16(b)))
+  if (!x || !W || !out || (ln && (!gamma || !beta)))
+    return lp_fail(EVO_E_INVALID, ln ? "x, gamma, beta, W and out are required"
+                                     : "x, W and out are required");
+  if (!al16(x) || !al16(W) || !al16(out) || (b && !al16(b)))
     return lp_fail(EVO_E_ALIGN, "tensors must be 16-byte aligned");
 
   LnProjArgs a{};
@@ -440,12 +446,13 @@ extern "C" evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void*
   a.N = d->N;
   a.NT = d->N % 256 == 0 ? 256 : (d->N % 128 == 0 ? 128 : 64);
   a.n_row_tiles = (int)((d->rows + 127) / 128);
+  a.ln = ln;
   a.eps = d->eps;
   a.gamma = gamma;
   a.beta = beta;
   a.b = b;
-  a.mean = mean;
-  a.rstd = rstd;
+  a.mean = ln ? mean : nullptr;
+  a.rstd = ln ? rstd : nullptr;
   CUtensorMap tx, tw, to;
   if (!make_2d_map(&tx, x, d->C, d->rows, d->x_ld, 128) ||
       !make_2d_map(&tw, W, d->C, d->N, d->C, a.NT / 2) ||
@@ -486,4 +493,16 @@ extern "C" evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void*
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? EVO_OK : lp_fail(EVO_E_CUDA, "ln_proj_fwd: %s", cudaGetErrorString(e));
+}
+
+extern "C" evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void* x,
+                                        const float* gamma, const float* beta, const void* W,
+                                        const float* b, void* out, float* mean, float* rstd,
+                                        void* stream) {
+  return ln_proj_launch(d, x, gamma, beta, W, b, out, mean, rstd, stream, 1);
+}
+
+extern "C" evo_status_t evo_linear_fwd(const evo_ln_proj_desc_t* d, const void* x, const void* W,
+                                       const float* b, void* out, void* stream) {
+  return ln_proj_launch(d, x, nullptr, nullptr, W, b, out, nullptr, nullptr, stream, 0);
 }

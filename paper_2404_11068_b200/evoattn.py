@@ -128,6 +128,8 @@ def load():
             lib.evo_global_attn_bwd.restype = i32
             lib.evo_ln_proj_fwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 9
             lib.evo_ln_proj_fwd.restype = i32
+            lib.evo_linear_fwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 5
+            lib.evo_linear_fwd.restype = i32
             _lib = lib
     return _lib
 
@@ -401,3 +403,19 @@ def ln_proj_fwd(x, gamma, beta, W, b=None, eps=1e-5, out=None, stream=None):
                                   _ptr(W.contiguous()), _ptr(b), _ptr(out), _ptr(mean),
                                   _ptr(rstd), _stream(stream)))
     return out, mean, rstd
+
+
+def linear_fwd(x, W, b=None, out=None, stream=None):
+    """out = x·Wᵀ + b on the tcgen05 projection kernel without the LayerNorm (evo_linear_fwd,
+    include/evo_ln_proj.h): e.g. the attention output projection.  x [rows, C] bf16; W [N, C]
+    bf16; b [N] fp32 or None."""
+    rows, C = x.shape
+    N = W.shape[0]
+    if out is None:
+        out = torch.empty((rows, N), dtype=torch.bfloat16, device=x.device)
+    d = LnProjDesc()
+    d.rows, d.C, d.N, d.eps = rows, C, N, 0.0
+    d.x_ld, d.out_ld = x.stride(0), out.stride(0)
+    _check(load().evo_linear_fwd(ctypes.byref(d), _ptr(x), _ptr(W.contiguous()), _ptr(b),
+                                 _ptr(out), _stream(stream)))
+    return out

@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from gpu_harness import rel_err
-from oracle.ln_proj import ln_qkvg_fwd
+from oracle.ln_proj import linear_fwd, ln_qkvg_fwd
 from paper_2404_11068_b200 import evoattn
 
 pytestmark = pytest.mark.gpu
@@ -83,3 +83,18 @@ def test_ln_proj_full_size_sampled():
                                     np.random.default_rng(0).integers(0, rows, 256)]))
     ref = _oracle(x, gamma, beta, W, b, C, N1, rows_idx=idx)
     assert rel_err(y.float().cpu().numpy()[idx], ref) < 2e-2
+
+
+@pytest.mark.parametrize("rows,C,N", [(300, 256, 256), (1000, 128, 128), (77, 64, 192)])
+def test_linear_parity(rows, C, N):
+    """Output projection (evo_linear_fwd): the gated attention output [rows, H·D] times W_oᵀ."""
+    g = torch.Generator(device="cpu").manual_seed(rows + N)
+    x = torch.randn((rows, C), generator=g).to(torch.bfloat16)
+    W = (torch.randn((N, C), generator=g) / C ** 0.5).to(torch.bfloat16)
+    b = torch.randn(N, generator=g)
+    dev = torch.device("cuda:0")
+    y = evoattn.linear_fwd(x.to(dev), W.to(dev), b.to(dev))
+    ref = linear_fwd(x.double().numpy(), W.double().numpy(), b.double().numpy())
+    assert rel_err(y.float().cpu().numpy(), ref) < 2e-2
+    y0 = evoattn.linear_fwd(x.to(dev), W.to(dev), None)
+    assert rel_err(y0.float().cpu().numpy(), ref - b.double().numpy()) < 2e-2

@@ -2,7 +2,7 @@
 import numpy as np
 import torch
 
-from oracle.ln_proj import ln_qkvg_fwd
+from oracle.ln_proj import linear_fwd, ln_qkvg_fwd
 
 
 def test_equals_torch_layer_norm_and_linear():
@@ -27,3 +27,13 @@ def test_identity_like_rows():
     y = (x - x.mean(1, keepdims=True)) / x.std(1, keepdims=True)
     for j in range(4):
         assert np.allclose(out[:, j], y @ W[:, j])
+
+
+def test_linear_unit_rows_and_additivity():
+    """Unit input rows select weight columns (x = I -> Wᵀ + b); the map is affine."""
+    r = np.random.default_rng(2)
+    W, b = r.standard_normal((6, 5)), r.standard_normal(6)
+    assert np.array_equal(linear_fwd(np.eye(5), W, b), W.T + b)
+    x1, x2 = r.standard_normal((3, 5)), r.standard_normal((3, 5))
+    lhs = linear_fwd(x1 + x2, W, b) - b
+    assert np.allclose(lhs, (linear_fwd(x1, W, b) - b) + (linear_fwd(x2, W, b) - b), atol=1e-12)
