@@ -10,6 +10,8 @@
 //   a13  bwd_bias  (CTA per (h, q tile, k tile, batch chunk)): dS recomputed, Σ_b dS held in
 //        registers over the chunk -> fp32 partials -> deterministic reduce (no atomics on dbias)
 //   a14  dq_convert: dq = bf16(scale · Σ dQ_part)
+#include <cstdlib>
+
 #include "evo_kernels.cuh"
 
 namespace evo {
@@ -164,10 +166,107 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const BwdPreArgs a) {
   }
 }
 
+// bf16 path, chunk per thread: NCH = D/8 consecutive lanes share a row, one 16-byte chunk each,
+// rows in the memory order of o (the smaller of its (h, l) strides fastest), so every warp-wide
+// load/store covers 512 contiguous bytes when the rows are dense; Σ_d dO·o by xor-shuffles inside
+// the row's lanes.  Two chunks per thread per iteration, all five loads in flight before the math.
+template <int NCH>
+__global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
+  const int Lq_pad = ((a.Lq + 127) / 128) * 128;
+  const bool hfast = a.o_sh < a.o_sl;
+  const float sgn = a.negate ? -1.f : 1.f;
+  const uint32_t H = (uint32_t)a.H, Lq = (uint32_t)a.Lq;
+  const uint32_t n = (uint32_t)a.B * H * Lq * NCH;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t c = threadIdx.x % NCH;
+  const __nv_bfloat16* o_p = reinterpret_cast<const __nv_bfloat16*>(a.o);
+  const __nv_bfloat16* d_p = reinterpret_cast<const __nv_bfloat16*>(a.dout);
+  const __nv_bfloat16* g_p = reinterpret_cast<const __nv_bfloat16*>(a.g);
+  for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += 2 * stride) {  // block-uniform trip
+    uint4 ov[2], dv[2], gv[2];
+    float l[2];
+    int64_t orow[2], grow[2], arow[2], vrow[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t idx = i0 + u * stride + threadIdx.x;
+      ok[u] = idx < n;
+      uint32_t r = (ok[u] ? idx : 0u) / NCH, h, q;
+      if (hfast) { h = r % H; r /= H; q = r % Lq; r /= Lq; }
+      else { q = r % Lq; r /= Lq; h = r % H; r /= H; }
+      const int64_t b = r;
+      orow[u] = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl + c * 8;
+      grow[u] = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl + c * 8;
+      arow[u] = b * a.a_sb + h * a.a_sh + (int64_t)q * a.a_sl + c * 8;
+      vrow[u] = (b * H + h) * Lq_pad + q;
+      ov[u] = dv[u] = gv[u] = make_uint4(0, 0, 0, 0);
+      l[u] = 0.f;
+      if (ok[u]) {
+        ov[u] = __ldg(reinterpret_cast<const uint4*>(o_p + orow[u]));
+        dv[u] = __ldg(reinterpret_cast<const uint4*>(d_p + orow[u]));
+        if (g_p) gv[u] = __ldg(reinterpret_cast<const uint4*>(g_p + grow[u]));
+        l[u] = __ldg(a.lse + (b * H + h) * Lq + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t ou[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
+      const uint32_t du[4] = {dv[u].x, dv[u].y, dv[u].z, dv[u].w};
+      const uint32_t gu[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+      uint32_t pa[4], pg[4];
+      float Dq = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float o0 = bf16_lo(ou[e]), o1 = bf16_hi(ou[e]);
+        const float d0v = bf16_lo(du[e]), d1v = bf16_hi(du[e]);
+        Dq = fmaf(d0v, o0, fmaf(d1v, o1, Dq));
+        const float s0 = 1.f / (1.f + __expf(-bf16_lo(gu[e])));
+        const float s1 = 1.f / (1.f + __expf(-bf16_hi(gu[e])));
+        pa[e] = pack_bf16(d0v * s0, d1v * s1);
+        pg[e] = pack_bf16(d0v * o0 * (1.f - s0), d1v * o1 * (1.f - s1));
+      }
+#pragma unroll
+      for (int m = 1; m < NCH; m <<= 1) Dq += __shfl_xor_sync(0xffffffffu, Dq, m);
+      if (!ok[u]) continue;
+      if (g_p) {
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow[u]) =
+            make_uint4(pa[0], pa[1], pa[2], pa[3]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dg) + grow[u]) =
+            make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      }
+      if (c == 0) {
+        a.Dvec[vrow[u]] = sgn * Dq;
+        a.lse2[vrow[u]] = sgn * (l[u] == -INFINITY ? INFINITY : l[u] * kLog2e);  // no kept key -> P = 0
+      }
+    }
+  }
+  // padding query rows [Lq, Lq_pad) of the statistics vectors: inert (D = 0, P = 0)
+  const uint32_t npad = (uint32_t)a.B * H * (uint32_t)(Lq_pad - a.Lq);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += stride) {
+    const uint32_t bh = i / (uint32_t)(Lq_pad - a.Lq), q = Lq + i % (uint32_t)(Lq_pad - a.Lq);
+    a.Dvec[(int64_t)bh * Lq_pad + q] = 0.f;
+    a.lse2[(int64_t)bh * Lq_pad + q] = sgn * INFINITY;
+  }
+}
+
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int Lq_pad = ((a.Lq + 127) / 128) * 128;
   const int64_t items = (int64_t)a.B * (Lq_pad / 32);
   if (items == 0) return cudaSuccess;
+  const int64_t nvec = (int64_t)a.B * a.H * Lq_pad * (a.D / 8);
+  static const bool old_pre = getenv("EVO_BWD_PRE_OLD") != nullptr;  // A/B switch
+  if (!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre) {
+    const int64_t blocks = (nvec + 511) / 512;  // two chunks per thread
+    const unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+    switch (a.D / 8) {
+      case 1: bwd_pre_vec_kernel<1><<<g, 256, 0, st>>>(a); break;
+      case 2: bwd_pre_vec_kernel<2><<<g, 256, 0, st>>>(a); break;
+      case 4: bwd_pre_vec_kernel<4><<<g, 256, 0, st>>>(a); break;
+      case 8: bwd_pre_vec_kernel<8><<<g, 256, 0, st>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   const unsigned g = (unsigned)(items < 148 * 6 ? items : 148 * 6);
   if (f32) {
     if (a.D <= 16) bwd_pre_kernel<true, 16><<<g, 256, 0, st>>>(a);
