@@ -491,15 +491,24 @@ __global__ void __launch_bounds__(384, 1)
         bulk_commit_group();
       }
     };
-    // hard-mask bit of this thread's key for batch row b (prefetched one batch row ahead)
-    auto load_keep = [&](int b) -> uint32_t {
-      if (kglob >= a.Lk || b >= a.B) return 0u;
-      return a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kglob * a.mask_s1] : 1u;
+    // hard-mask bits of this thread's key for 32 batch rows from b: all 32 byte loads in flight
+    // together, once per 32 rows (a per-row load was consumed right behind its issue)
+    auto load_keep_word = [&](int b) -> uint32_t {
+      if (kglob >= a.Lk) return 0u;
+      if (!a.mask) return ~0u;
+      uint32_t v[32];
+#pragma unroll
+      for (int x = 0; x < 32; ++x)
+        v[x] = b + x < b0 + nb ? (uint32_t)__ldg(a.mask + (int64_t)(b + x) * a.mask_s0 + (int64_t)kglob * a.mask_s1) : 0u;
+      uint32_t wd = 0u;
+#pragma unroll
+      for (int x = 0; x < 32; ++x) wd |= (v[x] != 0u ? 1u : 0u) << x;
+      return wd;
     };
     uint32_t pd_off[4];  // this thread's row of a [128][32] bf16 SW64 tile: 4 chunk offsets
 #pragma unroll
     for (int e = 0; e < 4; ++e) pd_off[e] = swz_offset(row, e, 64);
-    uint32_t keep_next = load_keep(b0);
+    uint32_t keep_word = 0u;
     bool keep = false;
     int bi = 0, t = 0, s = g;  // this group's sub-tiles: j = g, g+2, ...; j = ((bi*nq)+t)*4 + s
     for (int j = g; j < J; j += 2) {
@@ -507,8 +516,8 @@ __global__ void __launch_bounds__(384, 1)
       const int st = T & 1;
       const int b = b0 + bi;
       if (s == g && t == 0) {
-        keep = keep_next != 0u;
-        keep_next = load_keep(b + 1);
+        if ((bi & 31) == 0) keep_word = load_keep_word(b);
+        keep = (keep_word >> (bi & 31)) & 1u;
       }
       mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
       tc_fence_after();
