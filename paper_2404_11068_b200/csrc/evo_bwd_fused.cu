@@ -8,22 +8,22 @@
 // by the owning thread), so the separate dbias pass and its second recompute disappear.
 //
 // Roles (384 threads): two compute warpgroups (warps 0-3, 4-7) take alternate sub-tiles
-// (ping-pong: one group's exp/ALU work covers the other's hand-offs and drains); warps 8 and 11
-// (lane 0) issue the Sᵀ/dPᵀ MMAs of group 0 / group 1, warp 10 lane 0 the dV/dK/dQ MMAs, warp 9
-// lane 0 the TMA loads.  Thread = key row k = TMEM lane.
+// (ping-pong: one group's exp/ALU work covers the other's hand-offs and drains); warp 8 (lane 0)
+// issues the Sᵀ/dPᵀ MMAs of a sub-tile pair (one per group) as N = 64 MMAs, warp 10 lane 0 the
+// dV/dK/dQ MMAs, warp 9 lane 0 the TMA loads, warp 11 idles.  Thread = key row k = TMEM lane.
 // Per sub-tile j (queries q0..q0+31 of batch row b), group g = j & 1:
-//   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 32 queries) -> TMEM slot g
+//   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 32 queries of the pair) -> TMEM
 //   compute:  Pᵀ = exp2(Sᵀ·scale·log2e + biasᵀ·log2e − lse2), dSᵀ = Pᵀ⊙(dPᵀ − D)
 //             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ -> smem slot g, dSᵀ -> block (j & 3) of the tile
 //   MMA:      dV_b += Pᵀ·dA_j, dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a 128-query tile:
 //             dQ_part = dS·K_b (A = the tile's dSᵀ blocks read MN-major)
-// Group 0 also drains: at the first sub-tile of a query tile the previous tile's dQ part, at a
-// new batch row dK/dV, through swizzled staging tiles and TMA stores.
-// The issuer runs Sᵀ/dPᵀ ahead (one sub-tile per group), so before overwriting its Pᵀ slot a
+// Drains: group 1 the previous tile's dQ part at its first sub-tile of a query tile, group 0
+// dK/dV at a new batch row, through swizzled staging tiles and TMA stores.
+// The issuer runs Sᵀ/dPᵀ ahead (one sub-tile pair), so before overwriting its Pᵀ slot a
 // group waits for dV/dK(j-2) (bar_mm) and, at its first sub-tile of a tile, for the previous
 // tile's dQ MMA (bar_dq), the last reader of the dSᵀ blocks.
 //
-// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | 2 x (Sᵀ 32 | dPᵀ 32) | dV DP | dK DP | dQ DP
+// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | Sᵀ 2x32 | dPᵀ 2x32 | dV DP | dK DP | dQ DP
 // SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 |
 //       Q,dA x2 | Pᵀ x2 (8 KB) | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
 #include <cstdio>
@@ -157,52 +157,42 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (w == 8 || w == 11) {
-    // ------------------------------------------------------------------ Sᵀ/dPᵀ MMA issuers
+  } else if (w == 8) {
+    // ------------------------------------------------------------------ Sᵀ/dPᵀ MMA issuer
+    // One N = 64 MMA per K step covers the sub-tile pair (j, j+1) of the two groups (queries
+    // 32s..32s+63 of one tile, s in {0, 2}): a K = 16 step costs the same ~46 cycles at N = 32 and
+    // N = 64 (tools/micro/mma_bench.cu), so pairing halves the Sᵀ/dPᵀ tensor time.  TMEM slot
+    // layout [Sᵀ_j | Sᵀ_j+1 | dPᵀ_j | dPᵀ_j+1]; the pair starts once both groups pulled the
+    // previous pair (so it runs while they compute it).
     if (lane == 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 32, 0, 0);   // Sᵀ, dPᵀ
-      // Sᵀ/dPᵀ of sub-tile i+2 starts as soon as its group has pulled sub-tile i out of the TMEM
-      // slot (so it runs while that group computes i); dV/dK of sub-tile i once its Pᵀ/dSᵀ are
-      // in smem.  Per group sfree(i) < ps(i) < sfree(i+2), and the two groups run half a period
-      // apart, so this fixed blocking order never waits on an event that a later step produces.
-      auto issue_s = [&](int j, int bi, int t, int s) {
-        const int T = bi * nq + t, st = T & 1, kvs = bi & 1, g = j & 1;
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, 0, 0);
+      int sbi = 0, stt = 0, sss = 0;
+      for (int j = 0; j < J; j += 2) {
+        if (j >= 2) {
+          mbar_wait(bar_sfree, ((j - 2) >> 1) & 1);
+          mbar_wait(bar_sfree + 8, ((j - 2) >> 1) & 1);
+        }
+        const int T = sbi * nq + stt, st = T & 1, kvs = sbi & 1;
+        if (sss == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
+        if (sss == 0 && stt == 0) mbar_wait(bar_kv + 8 * kvs, (sbi >> 1) & 1);
         if (j < 256) DBG(2048 + j * 4 + 0);
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
-        const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + s * 32 * C::kRowBytes;
-        const uint32_t tS = tS0 + g * 64, tdP = tS + 32;
+        const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + sss * 32 * C::kRowBytes;
 #pragma unroll
         for (int kk = 0; kk < DP / 16; ++kk)
-          umma_bf16(tS, make_sdesc(kb + kk * 32, 16, 8 * C::kRowBytes, kSw),
+          umma_bf16(tS0, make_sdesc(kb + kk * 32, 16, 8 * C::kRowBytes, kSw),
                     make_sdesc(qb + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < DP / 16; ++kk)
-          umma_bf16(tdP, make_sdesc(kb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw),
+          umma_bf16(tS0 + 64, make_sdesc(kb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw),
                     make_sdesc(qb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s,
                     kk > 0);
-        umma_commit(bar_sp + 8 * g);
-      };
-      auto advance = [&](int& bi, int& t, int& s) {
-        if (++s == 4) {
-          s = 0;
-          if (++t == nq) { t = 0; ++bi; }
-        }
-      };
-      // one Sᵀ issuer per compute group (warp 8: even sub-tiles, warp 11: odd ones), so neither
-      // group's next Sᵀ waits on the other group's progress
-      const int gi = w == 8 ? 0 : 1;
-      int sbi = 0, stt = 0, sss = gi;
-      for (int j = gi; j < J; j += 2) {
-        if (j >= 2) mbar_wait(bar_sfree + 8 * gi, ((j - 2) >> 1) & 1);
-        // the first Sᵀ of this group in a tile / batch row waits for its inputs
-        const int T = sbi * nq + stt;
-        if (sss == gi) mbar_wait(bar_in + 8 * (T & 1), (T >> 1) & 1);
-        if (sss == gi && stt == 0) mbar_wait(bar_kv + 8 * (sbi & 1), (sbi >> 1) & 1);
-        issue_s(j, sbi, stt, sss);
+        umma_commit(bar_sp);
+        umma_commit(bar_sp + 8);
         sss += 2;
         if (sss >= 4) {
-          sss -= 4;
+          sss = 0;
           if (++stt == nq) { stt = 0; ++sbi; }
         }
       }
@@ -257,7 +247,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else {
+  } else if (w < 8) {  // (warp 11 idles)
     // ------------------------------------------------------------------ compute warpgroups
     const int g = w >> 2, qd = w & 3;
     const int row = qd * 32 + lane;  // key row within the tile = TMEM lane
@@ -527,9 +517,8 @@ __global__ void __launch_bounds__(384, 1)
       // one batch row ago): loaded with Sᵀ/dPᵀ so one wait covers all three
       uint32_t acc[32];
       {
-        const uint32_t tS = tS0 + g * 64;
-        tmem_ld32(tS + lane_base, rs);
-        tmem_ld32(tS + 32 + lane_base, rd);
+        tmem_ld32(tS0 + 32 * g + lane_base, rs);
+        tmem_ld32(tS0 + 64 + 32 * g + lane_base, rd);
         if (BIAS && bi > 0) tmem_ld32(tDB + lane_base + qcol, acc);
       }
       tmem_wait_ld();
