@@ -191,9 +191,14 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
     for (int u = 0; u < 2; ++u) {
       const uint32_t idx = i0 + u * stride + threadIdx.x;
       ok[u] = idx < n;
-      uint32_t r = (ok[u] ? idx : 0u) / NCH, h, q;
-      if (hfast) { h = r % H; r /= H; q = r % Lq; r /= Lq; }
-      else { q = r % Lq; r /= Lq; h = r % H; r /= H; }
+      uint32_t r = (ok[u] ? idx : 0u) / NCH, h, q, r2;
+      if (hfast) {
+        r2 = fdiv(r, a.fd_H); h = r - r2 * H; r = r2;
+        r2 = fdiv(r, a.fd_Lq); q = r - r2 * Lq; r = r2;
+      } else {
+        r2 = fdiv(r, a.fd_Lq); q = r - r2 * Lq; r = r2;
+        r2 = fdiv(r, a.fd_H); h = r - r2 * H; r = r2;
+      }
       const int64_t b = r;
       orow[u] = b * a.o_sb + h * a.o_sh + (int64_t)q * a.o_sl + c * 8;
       grow[u] = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl + c * 8;
@@ -220,8 +225,7 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
         const float o0 = bf16_lo(ou[e]), o1 = bf16_hi(ou[e]);
         const float d0v = bf16_lo(du[e]), d1v = bf16_hi(du[e]);
         Dq = fmaf(d0v, o0, fmaf(d1v, o1, Dq));
-        const float s0 = 1.f / (1.f + __expf(-bf16_lo(gu[e])));
-        const float s1 = 1.f / (1.f + __expf(-bf16_hi(gu[e])));
+        const float s0 = fast_sigmoid(bf16_lo(gu[e])), s1 = fast_sigmoid(bf16_hi(gu[e]));
         pa[e] = pack_bf16(d0v * s0, d1v * s1);
         pg[e] = pack_bf16(d0v * o0 * (1.f - s0), d1v * o1 * (1.f - s1));
       }
@@ -256,13 +260,16 @@ cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int64_t nvec = (int64_t)a.B * a.H * Lq_pad * (a.D / 8);
   static const bool old_pre = getenv("EVO_BWD_PRE_OLD") != nullptr;  // A/B switch
   if (!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre) {
+    BwdPreArgs v = a;
+    v.fd_H = make_fastdiv((uint32_t)a.H);
+    v.fd_Lq = make_fastdiv((uint32_t)a.Lq);
     const int64_t blocks = (nvec + 511) / 512;  // two chunks per thread
     const unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
     switch (a.D / 8) {
-      case 1: bwd_pre_vec_kernel<1><<<g, 256, 0, st>>>(a); break;
-      case 2: bwd_pre_vec_kernel<2><<<g, 256, 0, st>>>(a); break;
-      case 4: bwd_pre_vec_kernel<4><<<g, 256, 0, st>>>(a); break;
-      case 8: bwd_pre_vec_kernel<8><<<g, 256, 0, st>>>(a); break;
+      case 1: bwd_pre_vec_kernel<1><<<g, 256, 0, st>>>(v); break;
+      case 2: bwd_pre_vec_kernel<2><<<g, 256, 0, st>>>(v); break;
+      case 4: bwd_pre_vec_kernel<4><<<g, 256, 0, st>>>(v); break;
+      case 8: bwd_pre_vec_kernel<8><<<g, 256, 0, st>>>(v); break;
       default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -880,11 +887,16 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
   const bool hfast = a.q_sh < a.q_sl;
   (void)ND;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n8; idx += gridDim.x * blockDim.x) {
-    const uint32_t d0 = (idx % (uint32_t)nd) * 8;
-    uint32_t r = idx / (uint32_t)nd;
+    uint32_t r = fdiv(idx, a.fd_nd), r2;
+    const uint32_t d0 = (idx - r * (uint32_t)nd) * 8;
     uint32_t h, q;
-    if (hfast) { h = r % (uint32_t)a.H; r /= (uint32_t)a.H; q = r % (uint32_t)a.Lq; r /= (uint32_t)a.Lq; }
-    else { q = r % (uint32_t)a.Lq; r /= (uint32_t)a.Lq; h = r % (uint32_t)a.H; r /= (uint32_t)a.H; }
+    if (hfast) {
+      r2 = fdiv(r, a.fd_H); h = r - r2 * (uint32_t)a.H; r = r2;
+      r2 = fdiv(r, a.fd_Lq); q = r - r2 * (uint32_t)a.Lq; r = r2;
+    } else {
+      r2 = fdiv(r, a.fd_Lq); q = r - r2 * (uint32_t)a.Lq; r = r2;
+      r2 = fdiv(r, a.fd_H); h = r - r2 * (uint32_t)a.H; r = r2;
+    }
     const int64_t b = r;
     const float* src = a.acc + b * a.p_sb + (int64_t)h * a.p_sh + (int64_t)q * a.p_sl + d0;
     float4 x = __ldg(reinterpret_cast<const float4*>(src));
@@ -910,9 +922,13 @@ cudaError_t launch_dq_convert(const ConvertArgs& a, cudaStream_t st) {
   if (n8 >= (int64_t)1 << 31) return cudaErrorInvalidValue;
   const int64_t blocks = (n8 + 255) / 256;
   const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
-  if (a.D <= 16) dq_convert_kernel<16><<<g, 256, 0, st>>>(a);
-  else if (a.D <= 32) dq_convert_kernel<32><<<g, 256, 0, st>>>(a);
-  else dq_convert_kernel<64><<<g, 256, 0, st>>>(a);
+  ConvertArgs v = a;
+  v.fd_nd = make_fastdiv((uint32_t)((a.D + 7) / 8));
+  v.fd_H = make_fastdiv((uint32_t)a.H);
+  v.fd_Lq = make_fastdiv((uint32_t)a.Lq);
+  if (a.D <= 16) dq_convert_kernel<16><<<g, 256, 0, st>>>(v);
+  else if (a.D <= 32) dq_convert_kernel<32><<<g, 256, 0, st>>>(v);
+  else dq_convert_kernel<64><<<g, 256, 0, st>>>(v);
   return cudaGetLastError();
 }
 

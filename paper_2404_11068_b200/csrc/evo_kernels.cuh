@@ -4,6 +4,22 @@
 
 namespace evo {
 
+// Unsigned division by a runtime divisor d >= 1 without the integer-divide sequence (which goes
+// through the XU pipe): q = (umulhi(n, m) + n) >> l with l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1; exact for n < 2^31 (round-up method, Hacker's Delight 10-8).
+struct FastDiv {
+  uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.l = 0;
+  while ((1ull << f.l) < d) ++f.l;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << f.l) - d)) / d + 1);
+  return f;
+}
+EVO_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.m) + n) >> f.l; }
+
 // sets the thread-local text evo_last_error_detail() returns (evo_api.cu)
 void set_error_detail(const char* msg);
 
@@ -67,6 +83,7 @@ struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
   void* dA;      // dO·sigmoid(g) (NULL when no gate), element strides below, d unit-stride
   int64_t a_sb, a_sh, a_sl;
   int negate;    // store -lse2 and -D (the fused backward's operand form)
+  FastDiv fd_H, fd_Lq;  // filled by launch_bwd_pre
 };
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st);
 
@@ -183,6 +200,7 @@ struct ConvertArgs {  // dq = bf16(scale * Σ_p acc[p])
   int64_t p_sb, p_sh, p_sl;  // element strides of one part (d unit-stride)
   __nv_bfloat16* dq;
   int64_t q_sb, q_sh, q_sl;
+  FastDiv fd_nd, fd_H, fd_Lq;  // filled by launch_dq_convert
 };
 cudaError_t launch_dq_convert(const ConvertArgs& a, cudaStream_t st);
 
