@@ -779,8 +779,13 @@ cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, 
 
 // =============================================================================== reduce / convert
 // dbias[(b,) h, q, k] = Σ_c partial[c][(b,) h][q][k]   (partials padded to [.][Lq_pad][Lk_pad]).
-// Tiles of 32 q x 32 k: the partials are read along k (coalesced, 4 parts in flight) and the sum
-// is written along whichever of q/k is unit-stride in the destination (smem transpose for q).
+// Latency-bound (the partials are ~19 MB, ~0.13 MB per SM), so every thread issues the loads of
+// ALL its parts at once (NP >= nparts registers, predicated) and sums them in part order
+// (deterministic); no grid-stride loop, so the whole reduction is in flight.
+//
+// q-contiguous destination (end-node bias view): 32 q x 32 k tiles, 256 threads (4 rows each),
+// parts read along k (coalesced), transposed through shared memory, written along q.
+template <int NP>
 __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
   __shared__ float tile[32][33];
   const int Lq_pad = ((a.Lq + 127) / 128) * 128, Lk_pad = ((a.Lk + 127) / 128) * 128;
@@ -793,20 +798,22 @@ __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
   const int64_t bb = u / a.H;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const int k = kt * 32 + tx;
+  const float* src = a.partial + ((bb * a.H + h) * Lq_pad + qt * 32 + ty) * (int64_t)Lk_pad + k;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c0 = 0; c0 < a.nparts; c0 += NP) {  // one round unless nparts > NP
+    float v[4][NP];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int qi = ty + 8 * i, q = qt * 32 + qi;
-    const float* src = a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k;
-    float acc = 0.f;
-    for (int c0 = 0; c0 < a.nparts; c0 += 16) {  // up to 16 independent loads in flight
-      float v[16];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int c = 0; c < 16; ++c) v[c] = c0 + c < a.nparts ? src[(int64_t)(c0 + c) * plane] : 0.f;
+      for (int c = 0; c < NP; ++c)
+        v[i][c] = c0 + c < a.nparts ? __ldg(src + (int64_t)(8 * i) * Lk_pad + (int64_t)(c0 + c) * plane) : 0.f;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) acc += v[c];  // fixed order: deterministic
-    }
-    tile[qi][tx] = acc;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < NP; ++c) acc[i] += v[i][c];  // fixed order: deterministic
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tile[ty + 8 * i][tx] = acc[i];
   __syncthreads();
   if (a.q_fast) {  // destination q-contiguous: lanes along q
 #pragma unroll
@@ -827,37 +834,37 @@ __global__ void __launch_bounds__(256) dbias_reduce_kernel(const ReduceArgs a) {
 
 // k-contiguous destination (the common case): a thread per 4 consecutive keys of a row, every
 // part's float4 in flight before the (fixed-order) sum, one float4 store
+template <int NP>
 __global__ void __launch_bounds__(256) dbias_reduce_k4_kernel(const ReduceArgs a) {
   const int Lq_pad = ((a.Lq + 127) / 128) * 128, Lk_pad = ((a.Lk + 127) / 128) * 128;
   const int64_t plane = (int64_t)a.H * Lq_pad * Lk_pad;
   const int nk4 = (a.Lk + 3) / 4;
   const int64_t n = a.nb * a.H * (int64_t)a.Lq * nk4;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(idx % nk4) * 4;
-    int64_t t = idx / nk4;
-    const int q = (int)(t % a.Lq);
-    t /= a.Lq;
-    const int h = (int)(t % a.H);
-    const int64_t bb = t / a.H;
-    const float4* src = reinterpret_cast<const float4*>(
-        a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < a.nparts; c0 += 8) {
-      float4 v[8];
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const int k = (int)(idx % nk4) * 4;
+  int64_t t = idx / nk4;
+  const int q = (int)(t % a.Lq);
+  t /= a.Lq;
+  const int h = (int)(t % a.H);
+  const int64_t bb = t / a.H;
+  const float4* src = reinterpret_cast<const float4*>(
+      a.partial + ((bb * a.H + h) * Lq_pad + q) * (int64_t)Lk_pad + k);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = 0; c0 < a.nparts; c0 += NP) {  // one round unless nparts > NP
+    float4 v[NP];
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        v[c] = c0 + c < a.nparts ? src[(int64_t)(c0 + c) * (plane / 4)] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < NP; ++c)
+      v[c] = c0 + c < a.nparts ? __ldg(src + (int64_t)(c0 + c) * (plane / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) { acc.x += v[c].x; acc.y += v[c].y; acc.z += v[c].z; acc.w += v[c].w; }
-    }
-    float* dst = a.dbias + bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + k;
-    if (k + 3 < a.Lk && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-      *reinterpret_cast<float4*>(dst) = acc;
-    } else {
-      const float e4[4] = {acc.x, acc.y, acc.z, acc.w};
-      for (int e = 0; e < 4 && k + e < a.Lk; ++e) dst[e] = e4[e];
-    }
+    for (int c = 0; c < NP; ++c) { acc.x += v[c].x; acc.y += v[c].y; acc.z += v[c].z; acc.w += v[c].w; }
+  }
+  float* dst = a.dbias + bb * a.s_b + h * a.s_h + (int64_t)q * a.s_q + k;
+  if (k + 3 < a.Lk && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    *reinterpret_cast<float4*>(dst) = acc;
+  } else {
+    const float e4[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int e = 0; e < 4 && k + e < a.Lk; ++e) dst[e] = e4[e];
   }
 }
 
@@ -865,13 +872,16 @@ cudaError_t launch_dbias_reduce(const ReduceArgs& a, cudaStream_t st) {
   if (!a.q_fast && a.s_k == 1) {
     const int64_t n = a.nb * a.H * (int64_t)a.Lq * ((a.Lk + 3) / 4);
     if (n == 0) return cudaSuccess;
-    const int64_t blocks = (n + 255) / 256;
-    dbias_reduce_k4_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(a);
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (a.nparts <= 8) dbias_reduce_k4_kernel<8><<<blocks, 256, 0, st>>>(a);
+    else if (a.nparts <= 16) dbias_reduce_k4_kernel<16><<<blocks, 256, 0, st>>>(a);
+    else dbias_reduce_k4_kernel<32><<<blocks, 256, 0, st>>>(a);
     return cudaGetLastError();
   }
   const int64_t blocks = a.nb * a.H * (int64_t)((a.Lq + 31) / 32) * ((a.Lk + 31) / 32);
   if (blocks == 0) return cudaSuccess;
-  dbias_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  if (a.nparts <= 8) dbias_reduce_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else dbias_reduce_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(a);  // 4 rows x 16 in flight
   return cudaGetLastError();
 }
 
