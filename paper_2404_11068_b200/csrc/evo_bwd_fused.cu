@@ -14,8 +14,8 @@
 // Per sub-tile j (queries q0..q0+31 of batch row b), group g = j & 1:
 //   MMA:      Sᵀ = K_b·Q_jᵀ, dPᵀ = V_b·dA_jᵀ      (M = 128 keys, N = 32 queries of the pair) -> TMEM
 //   compute:  Pᵀ = exp2(Sᵀ·scale·log2e + biasᵀ·log2e − lse2), dSᵀ = Pᵀ⊙(dPᵀ − D)
-//             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ -> smem slot g, dSᵀ -> block (j & 3) of the tile
-//   MMA:      dV_b += Pᵀ·dA_j, dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a 128-query tile:
+//             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ -> TMEM slot g, dSᵀ -> smem block (j & 3) of the tile
+//   MMA:      dV_b += Pᵀ·dA_j (A = Pᵀ from TMEM), dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a tile:
 //             dQ_part = dS·K_b (A = the tile's dSᵀ blocks read MN-major)
 // Drains: group 1 the previous tile's dQ part at its first sub-tile of a query tile, group 0
 // dK/dV at a new batch row, through swizzled staging tiles and TMA stores.
@@ -23,9 +23,10 @@
 // group waits for dV/dK(j-2) (bar_mm) and, at its first sub-tile of a tile, for the previous
 // tile's dQ MMA (bar_dq), the last reader of the dSᵀ blocks.
 //
-// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | Sᵀ 2x32 | dPᵀ 2x32 | dV DP | dK DP | dQ DP
+// TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | Sᵀ 2x32 | dPᵀ 2x32 | dV DP | dK DP | dQ DP |
+//                  Pᵀ 2 x 16 (bf16 pairs)
 // SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 |
-//       Q,dA x2 | Pᵀ x2 (8 KB) | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
+//       Q,dA x2 | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
 #include <cstdio>
 #include <cstdlib>
 
@@ -41,8 +42,7 @@ struct FusedCfg {
   static constexpr uint32_t oBias = 0;
   static constexpr uint32_t oKV = oBias + kBiasMax;      // stage s: K at +s*2*kTile, V +kTile
   static constexpr uint32_t oQA = oKV + 4 * kTile;       // stage s: Q at +s*2*kTile, dA +kTile
-  static constexpr uint32_t oP = oQA + 4 * kTile;        // 2 x 8 KB  ([128 k][32 q], SW64)
-  static constexpr uint32_t oDS = oP + 16384;            // 4 x 8 KB  (one 128-query tile)
+  static constexpr uint32_t oDS = oQA + 4 * kTile;       // 4 x 8 KB  (one 128-query tile)
   static constexpr uint32_t oVec = oDS + 32768;          // 2 x (lse2[128], D[128]) fp32
   static constexpr uint32_t oStK = oVec + 2048;          // staging: dK, dV bf16, dQ bf16|fp32
   static constexpr uint32_t oStV = oStK + kTile;
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t cb = BIAS ? (uint32_t)Lq_pad : 0u;
   const uint32_t tDB = tmem, tS0 = tmem + cb, tdV = tS0 + 128, tdK = tdV + DP, tdQ = tdK + DP;
+  const uint32_t tP0 = tdQ + DP;  // Pᵀ slot g at +16 g (32 bf16 queries as 16 packed columns)
 
   if (w == 9) {
     // ------------------------------------------------------------------ TMA producer
@@ -215,13 +216,13 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
         const uint32_t ab = qb + C::kTile;
-        const uint32_t pb = s0 + C::oP + g * 8192, db = s0 + C::oDS + dss * 8192;
+        const uint32_t db = s0 + C::oDS + dss * 8192;
         const uint32_t acc0 = (dtt > 0 || dss > 0) ? 1u : 0u;
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk)  // dV += Pᵀ·dA (K = 32 queries)
-          umma_bf16(tdV, make_sdesc(pb + kk * 32, 16, 512, kSw64),
-                    make_sdesc(ab + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
-                    idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
+        for (int kk = 0; kk < 2; ++kk)  // dV += Pᵀ·dA (K = 32 queries; A = Pᵀ from TMEM)
+          umma_bf16_ts(tdV, tP0 + g * 16 + kk * 8,
+                       make_sdesc(ab + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
+                       idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)  // dK += dSᵀ·Q
           umma_bf16(tdK, make_sdesc(db + kk * 32, 16, 512, kSw64),
@@ -588,16 +589,16 @@ __global__ void __launch_bounds__(384, 1)
       if (s == g && T > 0) mbar_wait(bar_dq, (T - 1) & 1);
       tc_fence_after();
       const bool drain_now = g == 0 && s == 0 && j > 0;
-      // Pᵀ (slot g) and dSᵀ (block s) rows: this thread's key row, 32 queries = 4 x 16 B, SW64
+      // Pᵀ -> TMEM slot g (the A operand of the TS-form dV MMA); dSᵀ (block s) rows to smem:
+      // this thread's key row, 32 queries = 4 x 16 B, SW64
+      tmem_st16(tP0 + g * 16 + lane_base, pk);
       {
-        const uint32_t pb = s0 + C::oP + g * 8192, db = s0 + C::oDS + s * 8192;
+        const uint32_t db = s0 + C::oDS + s * 8192;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          st_shared_v4(pb + pd_off[e], pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        for (int e = 0; e < 4; ++e)
           st_shared_v4(db + pd_off[e], dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
-        }
       }
-      if (BIAS) tmem_wait_st();
+      tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();

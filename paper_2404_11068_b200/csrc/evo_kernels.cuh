@@ -167,7 +167,7 @@ struct BwdFusedLaunch {
 inline bool bwd_fused_supported(int DP, int Lq_pad, bool bias) {
   // the Σ_b dSᵀ accumulator needs Lq_pad TMEM columns (and the resident biasᵀ Lq_pad·256 B of
   // smem), so with a bias Lq <= 256; without one any Lq
-  const int cols = (bias ? Lq_pad : 0) + 128 + 3 * DP;
+  const int cols = (bias ? Lq_pad : 0) + 128 + 3 * DP + 32;  // Σ | Sᵀ,dPᵀ | dV dK dQ | Pᵀ x2
   return (!bias || Lq_pad <= 256) && cols <= 512 && (DP == 16 || DP == 32);
 }
 inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
