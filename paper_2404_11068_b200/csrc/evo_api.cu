@@ -149,13 +149,6 @@ bool use_fused_bwd(const evo_attn_desc_t* d) {
 }
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// dQ over DSMEM between the two key-tile CTAs (cluster of 2) instead of fp32 parts + dq_convert:
-// correct but slower in round 1 (the pair runs in lockstep), so opt-in: EVO_BWD_PAIRX=1
-bool pair_mode() {
-  const char* e = getenv("EVO_BWD_PAIRX");
-  return e && e[0] == '1';
-}
-
 WsLayout ws_layout(const evo_attn_desc_t* d) {
   WsLayout w;
   const int64_t nq = (d->Lq + 127) / 128, nk = (d->Lk + 127) / 128;
@@ -166,14 +159,11 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
   w.dvec = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   if (d->has_gate) { w.da = off; off = al256(off + (size_t)rows * d->Lq * d->D * esize(d)); }
   if (d->dtype == EVO_BF16 && nk > 1) {
-    // fused with > 2 key tiles: one fp32 dQ part per key tile (plain stores); split: one atomic
-    // sum; fused with exactly 2 key tiles sums the parts over DSMEM (no workspace)
+    // fused: one fp32 dQ part per key tile (plain stores); split: one atomic sum
     const bool fused = use_fused_bwd(d);
-    if (!(fused && nk == 2 && pair_mode())) {
-      w.dqacc = off;
-      const int64_t parts = fused ? nk : 1;
-      off = al256(off + (size_t)parts * rows * d->Lq * d->D * 4);
-    }
+    w.dqacc = off;
+    const int64_t parts = fused ? nk : 1;
+    off = al256(off + (size_t)parts * rows * d->Lq * d->D * 4);
   }
   w.fused = use_fused_bwd(d);
   if (d->dtype == EVO_BF16 && d->bias_kind != EVO_BIAS_NONE && d->B > 0) {
@@ -521,8 +511,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   const int bm = bias_mode(d);
   if (bm && !make_bias_map(&tb, d, bias)) return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
 
-  const bool pairx = W.fused && nk == 2 && pair_mode();
-  float* dqacc = (nk > 1 && !pairx) ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
+  float* dqacc = nk > 1 ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
   if (dqacc && !W.fused) {
     if ((e = cudaMemsetAsync(dqacc, 0, (size_t)d->B * d->H * d->Lq * d->D * 4, st)) != cudaSuccess)
       return cuda_fail(e, "memset dq_acc");
@@ -530,16 +519,15 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (W.fused) {
     evo::BwdFusedLaunch F;
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
-    // output maps for the TMA-store drains: dk/dv (bf16, k/v strides); dq (bf16, q strides)
-    // when there is one key tile, else the fp32 parts [nk*B][H][Lq][D] (32-column boxes)
-    const bool q_hfast = d->q_str[1] < d->q_str[2];  // parts follow dq's (h, l) order
+    // output maps of the dK/dV drains (bf16, k/v strides); the dQ parts (more than one key
+    // tile) are fp32, dense, in dq's (h, l) order (dq_convert reads them coalesced that way)
+    const bool q_hfast = d->q_str[1] < d->q_str[2];
     const int64_t part_str[3] = {(int64_t)d->H * d->Lq * d->D,
                                  q_hfast ? d->D : (int64_t)d->Lq * d->D,
                                  q_hfast ? (int64_t)d->H * d->D : d->D};
     if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str) ||
         !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str) ||
-        !((nk == 1 || pairx) ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str,
-                                           pairx ? 64 : 128)
+        !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str)
                   : make_x_map(&F.tm_dq, dqacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                (int64_t)nk * d->B, d->H, d->Lq, d->D, part_str, 128,
                                std::min(dpad(d->D), 32))))
@@ -558,7 +546,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dv = (__nv_bfloat16*)dv; fa.v_sb = d->v_str[0]; fa.v_sh = d->v_str[1]; fa.v_sl = d->v_str[2];
     fa.dq = (__nv_bfloat16*)dq; fa.q_sb = d->q_str[0]; fa.q_sh = d->q_str[1]; fa.q_sl = d->q_str[2];
     fa.dq_acc = dqacc;
-    fa.pairx = pairx ? 1 : 0;
+    fa.p_part = (int64_t)d->B * d->H * d->Lq * d->D;
+    fa.p_sb = part_str[0]; fa.p_sh = part_str[1]; fa.p_sl = part_str[2];
     static const int bwd_flags = getenv("EVO_BWD_FLAGS") ? atoi(getenv("EVO_BWD_FLAGS")) : 0;
     fa.flags = bwd_flags;
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;

@@ -17,16 +17,18 @@
 //             Σ_b dSᵀ += dSᵀ (TMEM RMW), Pᵀ -> TMEM slot g, dSᵀ -> smem block (j & 3) of the tile
 //   MMA:      dV_b += Pᵀ·dA_j (A = Pᵀ from TMEM), dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a tile:
 //             dQ_part = dS·K_b (A = the tile's dSᵀ blocks read MN-major)
-// Drains: group 1 the previous tile's dQ part at its first sub-tile of a query tile, group 0
-// dK/dV at a new batch row, through swizzled staging tiles and TMA stores.
-// The issuer runs Sᵀ/dPᵀ ahead (one sub-tile pair), so before overwriting its Pᵀ slot a
-// group waits for dV/dK(j-2) (bar_mm) and, at its first sub-tile of a tile, for the previous
-// tile's dQ MMA (bar_dq), the last reader of the dSᵀ blocks.
+// Drains: group 1 the previous tile's dQ part after its first sub-tile of a tile, group 0 dK/dV
+// at a new batch row, through swizzled staging tiles and TMA stores (direct per-thread global
+// stores of the rows measured ~10% slower).
+// The issuer runs Sᵀ/dPᵀ ahead (one sub-tile pair), so before overwriting its Pᵀ slot a group
+// waits for dV/dK(j-2) (bar_mm).  The dSᵀ blocks are double-buffered per 128-query tile (buffer
+// T & 1): a group starting tile T waits only for tile T-2's dQ MMA, long done, instead of the
+// previous tile's.
 //
 // TMEM (512 cols): [0, Lq_pad) Σ dSᵀ (with bias) | Sᵀ 2x32 | dPᵀ 2x32 | dV DP | dK DP | dQ DP |
 //                  Pᵀ 2 x 16 (bf16 pairs)
 // SMEM: biasᵀ resident [128 k][Lq_pad] bf16 (16-B chunks XOR-swizzled by k&7) | K,V x2 |
-//       Q,dA x2 | dSᵀ 4 x 8 KB | lse2/D x2 | dQ/dK/dV staging | barriers
+//       Q,dA x2 | dSᵀ 2 x 4 x 8 KB | lse2/D x2 | dK/dV/dQ staging | barriers
 #include <cstdio>
 #include <cstdlib>
 
@@ -42,13 +44,12 @@ struct FusedCfg {
   static constexpr uint32_t oBias = 0;
   static constexpr uint32_t oKV = oBias + kBiasMax;      // stage s: K at +s*2*kTile, V +kTile
   static constexpr uint32_t oQA = oKV + 4 * kTile;       // stage s: Q at +s*2*kTile, dA +kTile
-  static constexpr uint32_t oDS = oQA + 4 * kTile;       // 4 x 8 KB  (one 128-query tile)
-  static constexpr uint32_t oVec = oDS + 32768;          // 2 x (lse2[128], D[128]) fp32
+  static constexpr uint32_t oDS = oQA + 4 * kTile;       // 2 x 4 x 8 KB (tile T in buffer T & 1)
+  static constexpr uint32_t oVec = oDS + 65536;          // 2 x (lse2[128], D[128]) fp32
   static constexpr uint32_t oStK = oVec + 2048;          // staging: dK, dV bf16, dQ bf16|fp32
   static constexpr uint32_t oStV = oStK + kTile;
-  static constexpr uint32_t oStQ = oStV + kTile;
-  static constexpr uint32_t oRecv = oStQ + 128 * DP * 4;  // peer's dQ rows (64 x DP fp32)
-  static constexpr uint32_t oBar = oRecv + 64 * DP * 4;
+  static constexpr uint32_t oStQ = oStV + kTile;         // dQ staging: bf16 | fp32 [128][DP]
+  static constexpr uint32_t oBar = oStQ + 128 * DP * 4;
   static constexpr uint32_t kSmem = oBar + 256;
 };
 
@@ -78,20 +79,16 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t bar_sp = smem_u32(&bars[8]);       // +8: group 1   Sᵀ, dPᵀ in TMEM slot
   const uint32_t bar_sfree = smem_u32(&bars[10]);   // +8            group pulled its slot (4 warps)
   const uint32_t bar_ps = smem_u32(&bars[12]);      // +8            Pᵀ, dSᵀ in smem (4 warps)
-  const uint32_t bar_dq = smem_u32(&bars[14]);      // dQ MMA of a query tile (and all before) done
+  const uint32_t bar_dq = smem_u32(&bars[18]);      // +8: dSᵀ buffer 1   dQ MMA of a tile done
   const uint32_t bar_dkvfree = smem_u32(&bars[15]); // group 0 pulled a finished dK/dV (4 warps)
   const uint32_t bar_mm = smem_u32(&bars[16]);      // +8: group 1   dV/dK of its sub-tile done
-  const uint32_t bar_xfull = smem_u32(&bars[18]);   // pair: the peer's dQ rows landed (2 warps)
-  const uint32_t bar_xfree = smem_u32(&bars[19]);   // pair: the peer consumed ours (2 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[20]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
   const int Lq_pad = nq * 128, Lk_pad = nk * 128;
-  // pair mode: a cluster of 2 = the two key tiles of one (h, chunk); else (h, kt, chunk) flat
-  const int pr = a.pairx ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int c = a.pairx ? pr % a.nchunks : (int)blockIdx.x % a.nchunks;
-  const int grp = a.pairx ? (pr / a.nchunks) * 2 + (int)(blockIdx.x & 1) : (int)blockIdx.x / a.nchunks;
+  const int c = (int)blockIdx.x % a.nchunks;
+  const int grp = (int)blockIdx.x / a.nchunks;
   const int kt = grp % nk, h = grp / nk;
   const int k0 = kt * 128;
   const int b0 = c * a.chunk;
@@ -114,16 +111,12 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(bar_mm + 8 * i, 1);
     }
     mbar_init(bar_dq, 1);
+    mbar_init(bar_dq + 8, 1);
     mbar_init(bar_dkvfree, 4);
-    mbar_init(bar_xfull, 2);
-    mbar_init(bar_xfree, 2);
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
-  // pair mode: both CTAs of the cluster start their identical schedules together, so the dQ
-  // halves they exchange one sub-tile apart arrive before they are needed
-  if (a.pairx) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t cb = BIAS ? (uint32_t)Lq_pad : 0u;
@@ -216,7 +209,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
         const uint32_t ab = qb + C::kTile;
-        const uint32_t db = s0 + C::oDS + dss * 8192;
+        const uint32_t db = s0 + C::oDS + st * 32768 + dss * 8192;
         const uint32_t acc0 = (dtt > 0 || dss > 0) ? 1u : 0u;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)  // dV += Pᵀ·dA (K = 32 queries; A = Pᵀ from TMEM)
@@ -233,10 +226,10 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tdQ, make_sdesc(s0 + C::oDS + kk * 1024, 8192, 512, kSw64),
+            umma_bf16(tdQ, make_sdesc(s0 + C::oDS + st * 32768 + kk * 1024, 8192, 512, kSw64),
                       make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                       idesc_q, kk > 0 ? 1u : 0u);
-          umma_commit(bar_dq);
+          umma_commit(bar_dq + 8 * st);
           // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the groups' hand-offs;
           // dV/dK/dQ: this thread) is done once these commits land
           umma_commit(bar_infree + 8 * st);
@@ -339,111 +332,10 @@ __global__ void __launch_bounds__(384, 1)
                      pack_bf16(__uint_as_float(r[8 * i + 4]) * mul, __uint_as_float(r[8 * i + 5]) * mul),
                      pack_bf16(__uint_as_float(r[8 * i + 6]) * mul, __uint_as_float(r[8 * i + 7]) * mul));
     };
-    auto stage_f32 = [&](uint32_t base, const uint32_t (&r)[DP]) {
-#pragma unroll
-      for (int i = 0; i < DP / 4; ++i)
-        st_shared_v4(base + swz_offset(row, i, kRbF), r[4 * i], r[4 * i + 1], r[4 * i + 2],
-                     r[4 * i + 3]);
-    };
-    // dQ part of (bq, query tile at q0) and, if kv, dK/dV of batch row bk.  Called after the
-    // bar_dq wait (all MMAs up to that tile's dQ complete).  dK/dV are pulled first and released
-    // on bar_dkvfree (the next batch row's first dV/dK MMA overwrites them); the dQ part stays
-    // valid until the next tile's dQ MMA, which waits for this group's next hand-off.
-    // the thread that issues (and waits for) this CTA's TMA stores: in pair mode a thread of the
-    // 64-row half this CTA finalises
-    const int io_tid = a.pairx ? kt * 64 : 0;
-    // Drains (group 0).  dK/dV of batch row bk (kv); the dQ part of (bq, query tile at q0):
-    //  - single key tile: bf16 rows of the tile (dqmode 0)
-    //  - > 2 key tiles: this key tile's fp32 part (dqmode 0; dq_convert sums them)
-    //  - pair mode (2 key tiles, cluster of 2): CTA kt finalises rows [64·kt, 64·kt+64); at the
-    //    first sub-tile after the tile it SENDS the other half of its part to the peer over DSMEM
-    //    (dqmode 1), and one sub-tile later (dQ still in TMEM: the next dQ MMA waits for this
-    //    group's next hand-off) it ADDS the peer's half to its own and stores bf16 (dqmode 2), so
-    //    the peer's data has had a whole sub-tile to arrive.
-    auto drain = [&](int bq, int q0, bool kv, int bk, bool release_kv, int dqmode, int xt) {
-      const bool store_q = dqmode != 1;
-      if (kv || store_q) {
-        if (tid == io_tid) bulk_wait_group_read0();  // earlier stores left the staging tiles
-        named_bar_sync(2, 128);
-      }
-      uint32_t r[DP];
-      if (kv) {
-        tmem_ld_cols(tdK + lane_base, r);
-        tmem_wait_ld();
-        stage_bf16(s0 + C::oStK, r, a.scale);
-        tmem_ld_cols(tdV + lane_base, r);
-        tmem_wait_ld();
-        if (release_kv) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_dkvfree);
-        }
-        stage_bf16(s0 + C::oStV, r, 1.f);
-      }
-      constexpr uint32_t kRx = DP * 4;  // receive row bytes (fp32)
-      const int xrow = row & 63;
-      const bool mine = (qd >> 1) == kt;  // this thread's query row is in the half CTA kt owns
-      if (dqmode == 1) {
-        if (!mine) {
-          tmem_ld_cols(tdQ + lane_base, r);
-          tmem_wait_ld();
-          if (xt > 0) mbar_wait_cluster(bar_xfree, (xt - 1) & 1);
-          const uint32_t dst = mapa_shared(s0 + C::oRecv, (uint32_t)(kt ^ 1));
-#pragma unroll
-          for (int i = 0; i < DP / 4; ++i)
-            st_cluster_v4(dst + swz_offset(xrow, i, kRx), r[4 * i], r[4 * i + 1], r[4 * i + 2],
-                          r[4 * i + 3]);
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(mapa_shared(bar_xfull, (uint32_t)(kt ^ 1)));
-        }
-      } else if (dqmode == 2) {
-        if (mine) {
-          tmem_ld_cols(tdQ + lane_base, r);
-          tmem_wait_ld();
-          mbar_wait_cluster(bar_xfull, xt & 1);
-#pragma unroll
-          for (int i = 0; i < DP / 4; ++i) {
-            const uint4 v = ld_shared_v4(s0 + C::oRecv + swz_offset(xrow, i, kRx));
-            r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + __uint_as_float(v.x));
-            r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + __uint_as_float(v.y));
-            r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + __uint_as_float(v.z));
-            r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + __uint_as_float(v.w));
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(mapa_shared(bar_xfree, (uint32_t)(kt ^ 1)));
-#pragma unroll
-          for (int i = 0; i < DP / 8; ++i)
-            st_shared_v4(s0 + C::oStQ + swz_offset(xrow, i, kRbB),
-                         pack_bf16(__uint_as_float(r[8 * i]) * a.scale, __uint_as_float(r[8 * i + 1]) * a.scale),
-                         pack_bf16(__uint_as_float(r[8 * i + 2]) * a.scale, __uint_as_float(r[8 * i + 3]) * a.scale),
-                         pack_bf16(__uint_as_float(r[8 * i + 4]) * a.scale, __uint_as_float(r[8 * i + 5]) * a.scale),
-                         pack_bf16(__uint_as_float(r[8 * i + 6]) * a.scale, __uint_as_float(r[8 * i + 7]) * a.scale));
-        }
-      } else {
-        tmem_ld_cols(tdQ + lane_base, r);
-        tmem_wait_ld();
-        if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
-        else stage_f32(s0 + C::oStQ, r);
-      }
-      if (kv || store_q) {
-        fence_proxy_async_smem();
-        named_bar_sync(2, 128);
-        if (tid == io_tid) {
-          if (store_q) {
-            if (dqmode == 2) tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0 + 64 * kt, h, bq);
-            else tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
-          }
-          if (kv) {
-            tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
-            tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
-          }
-          bulk_commit_group();
-        }
-      }
-    };
-    // Split drains (default, no pair mode): group 0 drains dK/dV at a new batch row, group 1 the
-    // dQ part of the previous query tile, so the two groups share the drain work and group 0's
-    // dK/dV release (which gates the gradient issuer) is not queued behind the dQ store.
+    // Drains: group 0 drains dK/dV at a new batch row (staging + TMA stores), group 1 the dQ part
+    // of the previous query tile (straight from TMEM to global memory, each thread its own row),
+    // so the two groups share the drain work and group 0's dK/dV release (which gates the
+    // gradient issuer) is not queued behind the dQ store.
     auto drain_kv = [&](int bk, bool release_kv) {  // group 0
       if (tid == 0) bulk_wait_group_read0();
       named_bar_sync(2, 128);
@@ -467,18 +359,29 @@ __global__ void __launch_bounds__(384, 1)
         bulk_commit_group();
       }
     };
-    auto drain_q = [&](int bq, int q0) {  // group 1
+    // dQ part of tile Tq (group 1), once its dQ MMA has landed: bf16 rows when there is one key
+    // tile, else this key tile's fp32 part (dq_convert sums the parts); swizzled staging + TMA store
+    auto drain_q = [&](int Tq) {
+      mbar_wait(bar_dq + 8 * (Tq & 1), (Tq >> 1) & 1);
+      tc_fence_after();
       if (tid == 128) bulk_wait_group_read0();
       named_bar_sync(3, 128);
       uint32_t r[DP];
       tmem_ld_cols(tdQ + lane_base, r);
       tmem_wait_ld();
-      if (nk == 1) stage_bf16(s0 + C::oStQ, r, a.scale);
-      else stage_f32(s0 + C::oStQ, r);
+      if (nk == 1) {
+        stage_bf16(s0 + C::oStQ, r, a.scale);
+      } else {
+#pragma unroll
+        for (int i = 0; i < DP / 4; ++i)
+          st_shared_v4(s0 + C::oStQ + swz_offset(row, i, DP * 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                       r[4 * i + 3]);
+      }
       fence_proxy_async_smem();
       named_bar_sync(3, 128);
       if (tid == 128) {
-        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, q0, h, nk == 1 ? bq : kt * a.B + bq);
+        const int bq = b0 + Tq / nq;
+        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, (Tq % nq) * 128, h, nk == 1 ? bq : kt * a.B + bq);
         bulk_commit_group();
       }
     };
@@ -583,17 +486,16 @@ __global__ void __launch_bounds__(384, 1)
         }
         tmem_st32(tDB + lane_base + qcol, acc);
       }
-      // before overwriting: Pᵀ slot g is read by dV(j-2); the dSᵀ blocks of the previous tile by
-      // its dQ MMA (each group checks at its first sub-tile of a tile)
+      // before overwriting: Pᵀ slot g is read by dV(j-2); this tile's dSᵀ buffer (T & 1) by tile
+      // T-2's dQ MMA, long done (checked at the group's first sub-tile of a tile)
       if (j >= 2) mbar_wait(bar_mm + 8 * g, ((j - 2) >> 1) & 1);
-      if (s == g && T > 0) mbar_wait(bar_dq, (T - 1) & 1);
+      if (s == g && T >= 2) mbar_wait(bar_dq + 8 * st, ((T - 2) >> 1) & 1);
       tc_fence_after();
-      const bool drain_now = g == 0 && s == 0 && j > 0;
       // Pᵀ -> TMEM slot g (the A operand of the TS-form dV MMA); dSᵀ (block s) rows to smem:
       // this thread's key row, 32 queries = 4 x 16 B, SW64
       tmem_st16(tP0 + g * 16 + lane_base, pk);
       {
-        const uint32_t db = s0 + C::oDS + s * 8192;
+        const uint32_t db = s0 + C::oDS + st * 32768 + s * 8192;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           st_shared_v4(db + pd_off[e], dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
@@ -603,19 +505,15 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_ps + 8 * g);
-      if (!a.pairx) {
-        if (g == 0 && s == 0 && j > 0 && t == 0) drain_kv(b - 1, true);
-        if (g == 1 && s == 1 && T > 0) {
-          const int Tp = T - 1;
-          drain_q(b0 + Tp / nq, (Tp % nq) * 128);
-        }
-      } else if (drain_now) {  // pair mode: group 0 drains dQ (exchange) and dK/dV
-        const int Tp = T - 1;
-        drain(b0 + Tp / nq, (Tp % nq) * 128, t == 0, b - 1, true, a.pairx ? 1 : 0, Tp);
-      } else if (a.pairx && g == 0 && s == 2 && T > 0) {  // pair: finish the previous tile's dQ
-        const int Tp = T - 1;
-        drain(b0 + Tp / nq, (Tp % nq) * 128, false, 0, false, 2, Tp);
+      if (g == 0 && s == 0 && t == 0 && bi > 0) {
+        // the previous row's last dV/dK MMAs were group 1's sub-tile j - 1 (bar_mm slot 1)
+        mbar_wait(bar_mm + 8, ((j - 1) >> 1) & 1);
+        tc_fence_after();
+        drain_kv(b - 1, true);
       }
+      // the previous tile's dQ part; the next dQ MMA (which overwrites it) waits for this
+      // group's hand-off of the tile's last sub-tile
+      if (g == 1 && s == 1 && T > 0) drain_q(T - 1);
       s += 2;
       if (s >= 4) {
         s -= 4;
@@ -623,28 +521,15 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     // ---- tail: last dQ part (group 1) and last dK/dV (group 0); then both write Σ_b dSᵀ
-    if (!a.pairx) {
-      const int Tl = (J >> 2) - 1;
-      mbar_wait(bar_dq, Tl & 1);
+    const int Tl = (J >> 2) - 1;
+    if (g == 0) {
+      mbar_wait(bar_dq + 8 * (Tl & 1), (Tl >> 1) & 1);
       tc_fence_after();
-      if (g == 0) {
-        drain_kv(b0 + nb - 1, false);
-        if (tid == 0) bulk_wait_group0();
-      } else {
-        drain_q(b0 + Tl / nq, (Tl % nq) * 128);
-        if (tid == 128) bulk_wait_group0();
-      }
-    } else if (g == 0) {
-      const int Tl = (J >> 2) - 1;
-      mbar_wait(bar_dq, Tl & 1);
-      tc_fence_after();
-      if (a.pairx) {
-        drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false, 1, Tl);
-        drain(b0 + Tl / nq, (Tl % nq) * 128, false, 0, false, 2, Tl);
-      } else {
-        drain(b0 + Tl / nq, (Tl % nq) * 128, true, b0 + nb - 1, false, 0, Tl);
-      }
-      if (tid == io_tid) bulk_wait_group0();
+      drain_kv(b0 + nb - 1, false);
+      if (tid == 0) bulk_wait_group0();
+    } else {
+      drain_q(Tl);
+      if (tid == 128) bulk_wait_group0();
     }
     if (BIAS) {  // partial[c][h][q][k0 + row]: this group's 32-query column blocks
       float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
@@ -659,7 +544,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 #undef DBG
   tc_fence_before();
-  if (a.pairx) cluster_sync_all();  // no CTA leaves while its peer may still touch its smem
   __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
 }
@@ -673,31 +557,9 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
-  if (!L.args.pairx) {
-    kern<<<(unsigned)grid, 384, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
-                                            L.tm_dv, L.args);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(384);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (getenv("EVO_DEBUG_CLUSTERS")) {
-    int ncl = 0;
-    cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
-    fprintf(stderr, "bwd_fused pair mode: grid %lld CTAs = %lld clusters, max active %d\n", grid,
-            grid / 2, ncl);
-  }
-  return cudaLaunchKernelEx(&cfg, kern, L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk, L.tm_dv,
-                            L.args);
+  kern<<<(unsigned)grid, 384, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk, L.tm_dv,
+                                          L.args);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {

@@ -152,10 +152,10 @@ struct BwdFusedArgs {
   int64_t v_sb, v_sh, v_sl;
   __nv_bfloat16* dq;  // direct store when there is a single key tile
   int64_t q_sb, q_sh, q_sl;
-  float* dq_acc;      // otherwise [nk][B,H,Lq,D] fp32: key tile kt's dQ part (plain stores)
+  float* dq_acc;      // otherwise nk fp32 parts: key tile kt's dQ part (plain stores) at
+  int64_t p_part, p_sb, p_sh, p_sl;  // dq_acc + kt*p_part + b*p_sb + h*p_sh + q*p_sl
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
   unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
-  int pairx;  // two key tiles: CTA pair (cluster of 2) sums dQ over DSMEM, bf16 dq via TMA
   int flags;  // experiment switches (EVO_BWD_FLAGS), 0 in production
 };
 struct BwdFusedLaunch {

@@ -109,13 +109,12 @@ def test_gradient_identities():
 
 
 @pytest.mark.parametrize("bias_t", [False, True])
-def test_bf16_parity_pair_mode(monkeypatch, bias_t):
-    """The opt-in cluster-pair dQ exchange of the fused backward (EVO_BWD_PAIRX=1, two key
-    tiles) against the oracle."""
-    monkeypatch.setenv("EVO_BWD_PAIRX", "1")
+def test_bf16_parity_two_key_tiles(bias_t):
+    """Two key tiles (fp32 dQ parts of the fused backward summed by dq_convert), k- and
+    q-contiguous bias, against the oracle."""
     errs, _, _ = run_case(3, 2, 256, 256, 32, seed=5, bias="shared", bias_t=bias_t, gate=True,
                           mask="prefix", mask_t=False, layout="blhd")
-    _assert(errs, torch.bfloat16, f"pair mode bias_t={bias_t}")
+    _assert(errs, torch.bfloat16, f"two key tiles bias_t={bias_t}")
 
 
 @pytest.mark.parametrize("B,H,L,bias", [(64, 8, 64, None), (64, 8, 32, None), (40, 2, 256, "shared"),
