@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(128, 4)
     if (!all_kept) { mw0 = smask[2 * c]; mw1 = smask[2 * c + 1]; }
     mbar_wait(bar_s, c & 1);
     tc_fence_after();
+    if (tid == 0 && c >= 1 && c - 1 + C::kNSt < nc) {
+      // PV_{c-1} has landed (it precedes S_c in the MMA pipe): chunk c-1's stage is free
+      mbar_wait(bar_o, (c - 1) & 1);
+      load_chunk(c - 1 + C::kNSt);
+    }
     float x[64];
     {
       uint32_t r0[32], r1[32];
@@ -233,8 +238,8 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
       for (int i = 0; i < 4; ++i) m4[i] = fmax3(m4[i], x[k + i], x[k + 4 + i]);
     const float mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
-    // lazy online-softmax rescale (threshold 8 in log2 units); PV_{c-1} is complete here
-    // (S_c was issued only after it), so O may be touched directly
+    // lazy online-softmax rescale (threshold 8 in log2 units); PV_{c-1} is complete here (S_c
+    // was issued after it and the MMA pipe executes in order), so O may be touched directly
     const float m_new = fmaxf(m_ref, mx);
     if (c == 0) {
       m_ref = m_new;
@@ -286,9 +291,8 @@ __global__ void __launch_bounds__(128, 4)
                      idesc_o, (c > 0 || kk > 0) ? 1u : 0u);
       umma_commit(bar_o);
       if (c + 1 < nc) {
-        // S_{c+1} overwrites the P columns: wait for PV_c, which also frees stage `st`
-        mbar_wait(bar_o, c & 1);
-        if (c + C::kNSt < nc) load_chunk(c + C::kNSt);
+        // S_{c+1} overwrites the P columns PV_c reads: tcgen05.mma executes in issue order, so
+        // it is issued right behind PV_c (no wait for PV_c on the critical path)
         mbar_wait(bar_kv0 + 8 * ((c + 1) % C::kNSt), ((c + 1) / C::kNSt) & 1);
         issue_S(c + 1);
       }
