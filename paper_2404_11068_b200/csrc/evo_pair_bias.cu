@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -157,6 +158,103 @@ __global__ void __launch_bounds__(256) pair_bias_fwd_kernel(const PbArgs a) {
   }
 }
 
+// Two threads per pair row (lanes 2t, 2t+1 take the two channel halves), one pass over z (the
+// forward the bench path uses).  With G[c,h] = γ_c·W[c,h], gsum_h = Σ_c G[c,h] and
+// bsum_h = Σ_c β_c·W[c,h] (per block, from W/γ/β in shared memory):
+//   bias_h = Σ_c ((z_c − mean)·rstd·γ_c + β_c)·W[c,h] = rstd·(Σ_c z_c·G[c,h] − mean·gsum_h) + bsum_h
+// so the row is read once, as the statistics are (the paper's single-pass LN):
+// each thread issues all its 16-byte loads first (before the block's parameter set-up, so their
+// latency covers it), then accumulates Σz, Σz² and the H dot products, and the lane pair combines
+// them with one xor-shuffle each.  Consecutive pairs take consecutive j, so the head-major bias
+// (j unit-stride) and mean/rstd leave as coalesced stores.
+template <int C, int H>
+__global__ void __launch_bounds__(256) pair_bias_fwd_row_kernel(const PbArgs a, const FastDiv fd_Lj) {
+  // G[c][h] with the second channel half shifted by 4 floats: the two halves of a lane pair read
+  // channels c and c + C/2 at the same time, which would otherwise share banks
+  constexpr int kHalfOff = C / 2 * H + 4;
+  __shared__ __align__(16) float sG[2 * kHalfOff];
+  __shared__ float sBW[C][H];   // β_c·W[c,h]
+  __shared__ float sSum[2][H];  // gsum, bsum
+  constexpr int NCH = C / 16;   // 16-byte chunks per half row
+  const uint32_t nrows = (uint32_t)(a.Li * a.Lj);
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 1;
+  const int half = threadIdx.x & 1;
+  const bool ok = r < nrows;
+  const uint32_t i = fdiv(ok ? r : 0u, fd_Lj), j = (ok ? r : 0u) - i * (uint32_t)a.Lj;
+  uint4 u[NCH];
+  {
+    const uint4* zp = reinterpret_cast<const uint4*>(a.z + (int64_t)i * a.z_si + (int64_t)j * a.z_sj) +
+                      half * NCH;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) u[k] = ok ? __ldg(zp + k) : make_uint4(0, 0, 0, 0);
+  }
+  for (int x = threadIdx.x; x < C * H; x += blockDim.x) {
+    const int c = x / H;
+    const float wv = a.W[x];
+    sG[(c >= C / 2) * kHalfOff + (c % (C / 2)) * H + x % H] = a.gamma[c] * wv;
+    sBW[c][x % H] = a.beta[c] * wv;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * H) {  // gsum_h, bsum_h: column sums of the tables, fixed channel order
+    const int h = threadIdx.x % H;
+    const bool isb = threadIdx.x >= H;
+    auto tab = [&](int c) {
+      return isb ? sBW[c][h] : sG[(c >= C / 2) * kHalfOff + (c % (C / 2)) * H + h];
+    };
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < C; c += 4) {
+      t0 += tab(c);
+      t1 += tab(c + 1);
+      t2 += tab(c + 2);
+      t3 += tab(c + 3);
+    }
+    sSum[threadIdx.x >= H][h] = (t0 + t1) + (t2 + t3);
+  }
+  __syncthreads();
+  // Σz, Σz² and the dot products in packed fp32 pairs (FFMA2): dot2[p] holds heads 2p, 2p+1
+  uint64_t st2 = 0, dot2[H / 2];
+#pragma unroll
+  for (int p2 = 0; p2 < H / 2; ++p2) dot2[p2] = 0;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const uint32_t w4[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float z = (e & 1) ? bf16_hi(w4[e >> 1]) : bf16_lo(w4[e >> 1]);
+      const uint64_t zz = f2_pack(z, z);
+      st2 = f2_fma(zz, f2_pack(1.f, z), st2);  // (Σz, Σz²)
+      const uint4* g = reinterpret_cast<const uint4*>(sG + half * kHalfOff + (k * 8 + e) * H);
+#pragma unroll
+      for (int q = 0; q < H / 4; ++q) {
+        const uint4 gv = g[q];
+        dot2[2 * q] = f2_fma(zz, ((uint64_t)gv.y << 32) | gv.x, dot2[2 * q]);
+        dot2[2 * q + 1] = f2_fma(zz, ((uint64_t)gv.w << 32) | gv.z, dot2[2 * q + 1]);
+      }
+    }
+  }
+  float s, ss, dot[H];
+  f2_unpack(st2, s, ss);
+#pragma unroll
+  for (int p2 = 0; p2 < H / 2; ++p2) f2_unpack(dot2[p2], dot[2 * p2], dot[2 * p2 + 1]);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+#pragma unroll
+  for (int h = 0; h < H; ++h) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], 1);
+  if (!ok) return;
+  const float mean = s * (1.f / C);
+  const float rstd = rsqrtf(fmaxf(ss * (1.f / C) - mean * mean, 0.f) + a.eps);
+#pragma unroll
+  for (int h = 0; h < H; ++h)  // the pair splits the heads' stores
+    if ((h & 1) == half)
+      a.bias[h * a.b_sh + (int64_t)i * a.b_si + (int64_t)j * a.b_sj] =
+          __float2bfloat16_rn(fmaf(rstd, dot[h] - mean * sSum[0][h], sSum[1][h]));
+  if (half == 0) {
+    a.mean[r] = mean;
+    a.rstd[r] = rstd;
+  }
+}
+
 // ------------------------------------------------------------------ backward
 // Same warp-per-row walk; every lane accumulates the parameter gradients of its NC channels over
 // the warp's rows in registers (dW NC x H, dγ, dβ), the block's 8 warps are summed in a fixed
@@ -292,6 +390,16 @@ inline int64_t pb_warps(const PbArgs& a) { return (a.Li * a.Lj + kRowsPerWarp - 
 
 template <int C>
 static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
+  const int64_t rows = a.Li * a.Lj;
+  static const bool warp_rows = getenv("EVO_PB_FWD_WARP") != nullptr;  // A/B: warp-per-row kernel
+  if (!warp_rows && rows < ((int64_t)1 << 31)) {
+    const unsigned grid = (unsigned)((rows + 127) / 128);  // 128 rows (two threads each) per block
+    const FastDiv fd = make_fastdiv((uint32_t)a.Lj);
+    if (a.H == 4) pair_bias_fwd_row_kernel<C, 4><<<grid, 256, 0, st>>>(a, fd);
+    else if (a.H == 8) pair_bias_fwd_row_kernel<C, 8><<<grid, 256, 0, st>>>(a, fd);
+    else pair_bias_fwd_row_kernel<C, 16><<<grid, 256, 0, st>>>(a, fd);
+    return cudaGetLastError();
+  }
   const int64_t warps = (a.Li * a.Lj + kFwdRowsPerWarp - 1) / kFwdRowsPerWarp;
   const unsigned grid = (unsigned)((warps + 7) / 8);
   if (a.H == 4) pair_bias_fwd_kernel<C, 4><<<grid, 256, 0, st>>>(a);
