@@ -363,23 +363,33 @@ __global__ void __launch_bounds__(256) pair_bias_bwd_kernel(const PbArgs a) {
   }
 }
 
-// step 2 of the parameter-gradient reduction: column sums over the block partials, fixed order
-__global__ void __launch_bounds__(256) pair_bias_reduce_kernel(const float* __restrict__ part,
-                                                               int nblocks, int nout, int C, int H,
-                                                               float* dW, float* dgamma,
-                                                               float* dbeta) {
-  __shared__ float red[8][33];
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int wv = threadIdx.x >> 5;
+// step 2 of the parameter-gradient reduction: column sums over the block partials, fixed order.
+// 32 columns x 32 partial groups per 1024-thread block: each thread sums its group's partials
+// (8 loads in flight per round), then the 32 group sums of a column are added in order.
+__global__ void __launch_bounds__(1024) pair_bias_reduce_kernel(const float* __restrict__ part,
+                                                                int nblocks, int nout, int C, int H,
+                                                                float* dW, float* dgamma,
+                                                                float* dbeta) {
+  __shared__ float red[32][33];
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + col;
+  const int per = (nblocks + 31) / 32, b0 = grp * per, b1 = min(nblocks, b0 + per);
   float acc = 0.f;
-  if (o < nout)
-    for (int b = wv; b < nblocks; b += 8) acc += part[(int64_t)b * nout + o];
-  red[wv][threadIdx.x & 31] = acc;
+  if (o < nout) {
+    for (int b = b0; b < b1; b += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = b + k < b1 ? __ldg(part + (int64_t)(b + k) * nout + o) : 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+  }
+  red[grp][col] = acc;
   __syncthreads();
-  if (wv == 0 && o < nout) {
+  if (grp == 0 && o < nout) {
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x & 31];
+    for (int k = 0; k < 32; ++k) t += red[k][col];
     if (o < C * H) dW[o] = t;
     else if (o < C * H + C) dgamma[o - C * H] = t;
     else dbeta[o - C * H - C] = t;
@@ -536,8 +546,8 @@ evo_status_t evo_pair_bias_bwd(const evo_pair_bias_desc_t* d, const void* z, con
   cudaError_t e = launch_bwd(a, st);
   if (e != cudaSuccess) return pb_fail(EVO_E_CUDA, "pair_bias_bwd: %s", cudaGetErrorString(e));
   const int nb = (int)bwd_blocks(d);
-  evo::pair_bias_reduce_kernel<<<(nout + 31) / 32, 256, 0, st>>>(a.partial, nb, nout, d->C, d->H,
-                                                                 dW, dgamma, dbeta);
+  evo::pair_bias_reduce_kernel<<<(nout + 31) / 32, 1024, 0, st>>>(a.partial, nb, nout, d->C, d->H,
+                                                                  dW, dgamma, dbeta);
   e = cudaGetLastError();
   return e == cudaSuccess ? EVO_OK : pb_fail(EVO_E_CUDA, "pair_bias_reduce: %s", cudaGetErrorString(e));
 }
