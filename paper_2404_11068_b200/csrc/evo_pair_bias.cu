@@ -363,6 +363,143 @@ __global__ void __launch_bounds__(256) pair_bias_bwd_kernel(const PbArgs a) {
   }
 }
 
+// Backward for C <= 128, 128 pair rows per 256-thread block, in two phases:
+//  1. two threads per row (channel halves, as the forward): ẑ from z/mean/rstd, dy_c = Σ_h dbias_h·W[c,h]
+//     (W from shared memory), g = dy·γ, the row sums Σg and Σg·ẑ (one xor-shuffle), then
+//     dz_c = rstd·(g_c − Σg/C − ẑ_c·Σgẑ/C) straight to global memory (16-byte stores); ẑ and the row's
+//     dbias go to shared memory;
+//  2. one thread per (channel, half of the rows): the block's parameter-gradient partials
+//     dW[c,h] = Σ_r y·dbias_h, dγ_c = Σ_r dy·ẑ, dβ_c = Σ_r dy from the staged ẑ/dbias (W row in
+//     registers), the two row halves added in a fixed order; pair_bias_reduce_kernel sums the block
+//     partials (the paper's two-step reduction; deterministic, no atomics).
+// The rows' dbias values (consecutive j) and z loads are coalesced; no per-row warp reductions.
+template <int C, int H>
+__global__ void __launch_bounds__(256) pair_bias_bwd_row_kernel(const PbArgs a, const FastDiv fd_Lj) {
+  constexpr int ROWS = 128, NCH = C / 16, CH = C / 2;  // chunks / channels per thread
+  constexpr int kHalfOff = CH * H + 4;                  // bank-shifted halves of the W table
+  constexpr int ZS = C + 1;                             // padded ẑ row stride (conflict-free)
+  extern __shared__ __align__(16) float sm[];
+  float* sW = sm;                        // [2 * kHalfOff]
+  float* sZ = sW + 2 * kHalfOff;         // [ROWS][ZS]
+  float* sDB = sZ + ROWS * ZS;           // [ROWS][H]
+  float* sRed = sDB + ROWS * H;          // [C][H + 2] (phase-2 partials of the second row half)
+  const int tid = threadIdx.x;
+  const uint32_t nrows = (uint32_t)(a.Li * a.Lj);
+  const int lrow = tid >> 1, half = tid & 1;
+  const uint32_t r = blockIdx.x * ROWS + lrow;
+  const bool ok = r < nrows;
+  const uint32_t i = fdiv(ok ? r : 0u, fd_Lj), j = (ok ? r : 0u) - i * (uint32_t)a.Lj;
+  // ---- phase 1 loads first (their latency covers the W table set-up)
+  uint4 u[NCH];
+  float db[H], mean = 0.f, rstd = 0.f;
+  {
+    const uint4* zp = reinterpret_cast<const uint4*>(a.z + (int64_t)i * a.z_si + (int64_t)j * a.z_sj) +
+                      half * NCH;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) u[k] = ok ? __ldg(zp + k) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int h = 0; h < H; ++h) db[h] = ok ? __ldg(a.dbias + h * a.b_sh + (int64_t)i * a.b_si + (int64_t)j * a.b_sj) : 0.f;
+    if (ok) { mean = __ldg(a.mean + r); rstd = __ldg(a.rstd + r); }
+  }
+  for (int x = tid; x < C * H; x += blockDim.x) {
+    const int c = x / H;
+    sW[(c >= CH) * kHalfOff + (c % CH) * H + x % H] = a.W[x];
+  }
+  __syncthreads();
+  const float* wt = sW + half * kHalfOff;
+  const float* gm = a.gamma + half * CH;
+  float sg = 0.f, sgz = 0.f;
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const uint32_t w4[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = k * 8 + e;
+      const float zh = (((e & 1) ? bf16_hi(w4[e >> 1]) : bf16_lo(w4[e >> 1])) - mean) * rstd;
+      float dy = 0.f;
+#pragma unroll
+      for (int h = 0; h < H; ++h) dy = fmaf(db[h], wt[c * H + h], dy);
+      const float g = dy * __ldg(gm + c);
+      sg += g;
+      sgz = fmaf(g, zh, sgz);
+      sZ[lrow * ZS + half * CH + c] = zh;
+    }
+  }
+  sg += __shfl_xor_sync(0xffffffffu, sg, 1);
+  sgz += __shfl_xor_sync(0xffffffffu, sgz, 1);
+  sg *= 1.f / C;
+  sgz *= 1.f / C;
+  if (ok) {
+    __nv_bfloat16* dzp = a.dz + (int64_t)i * a.z_si + (int64_t)j * a.z_sj + half * CH;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+        float d2[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c = k * 8 + 2 * e2 + t;
+          const float zh = sZ[lrow * ZS + half * CH + c];
+          float dy = 0.f;
+#pragma unroll
+          for (int h = 0; h < H; ++h) dy = fmaf(db[h], wt[c * H + h], dy);
+          d2[t] = rstd * (dy * __ldg(gm + c) - sg - zh * sgz);
+        }
+        pk[e2] = pack_bf16(d2[0], d2[1]);
+      }
+      *reinterpret_cast<uint4*>(dzp + k * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+  if (half == 0) {
+#pragma unroll
+    for (int h = 0; h < H; ++h) sDB[lrow * H + h] = db[h];  // 0 for rows past the end
+  }
+  __syncthreads();
+  // ---- phase 2: thread (c, row half) accumulates the block's parameter gradients
+  const int c = tid % C, rh = tid / C;  // 256 threads: C = 128 -> 2 row halves, C = 64 -> 4, ...
+  constexpr int NRH = 256 / C;
+  float wc[H], dw[H], dg = 0.f, dbt = 0.f;
+#pragma unroll
+  for (int h = 0; h < H; ++h) { wc[h] = a.W[c * H + h]; dw[h] = 0.f; }
+  const float gc = a.gamma[c], bc = a.beta[c];
+  const int nr = (int)min((uint32_t)ROWS, nrows - blockIdx.x * ROWS);
+  for (int rr = rh; rr < nr; rr += NRH) {
+    const float zh = sZ[rr * ZS + c];
+    const float y = fmaf(zh, gc, bc);
+    float dy = 0.f;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const float dbh = sDB[rr * H + h];
+      dy = fmaf(dbh, wc[h], dy);
+      dw[h] = fmaf(y, dbh, dw[h]);
+    }
+    dg = fmaf(dy, zh, dg);
+    dbt += dy;
+  }
+  // fixed-order combination of the row groups through shared memory (reusing sZ)
+  __syncthreads();
+  float* red = sZ;  // [NRH][C][H + 2]
+#pragma unroll
+  for (int h = 0; h < H; ++h) red[(rh * C + c) * (H + 2) + h] = dw[h];
+  red[(rh * C + c) * (H + 2) + H] = dg;
+  red[(rh * C + c) * (H + 2) + H + 1] = dbt;
+  __syncthreads();
+  if (rh == 0) {
+    float* part = a.partial + (int64_t)blockIdx.x * (C * H + 2 * C);
+#pragma unroll
+    for (int h = 0; h < H + 2; ++h) {
+      float t = 0.f;
+#pragma unroll
+      for (int g2 = 0; g2 < NRH; ++g2) t += red[(g2 * C + c) * (H + 2) + h];
+      if (h < H) part[c * H + h] = t;
+      else if (h == H) part[C * H + c] = t;
+      else part[C * H + C + c] = t;
+    }
+  }
+  (void)sRed;
+}
+
 // step 2 of the parameter-gradient reduction: column sums over the block partials, fixed order.
 // 32 columns x 32 partial groups per 1024-thread block: each thread sums its group's partials
 // (8 loads in flight per round), then the 32 group sums of a column are added in order.
@@ -420,6 +557,19 @@ static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
 
 template <int C, int H>
 static cudaError_t launch_bwd_ch(const PbArgs& a, cudaStream_t st) {
+  static const bool warp_rows = getenv("EVO_PB_BWD_WARP") != nullptr;  // A/B: warp-per-row kernel
+  if constexpr (C <= 128) {
+    if (!warp_rows && a.Li * a.Lj < ((int64_t)1 << 31)) {
+      // 128 rows per block: the same block count (and partial layout) as the warp kernel
+      const unsigned grid = (unsigned)((a.Li * a.Lj + 127) / 128);
+      auto k = pair_bias_bwd_row_kernel<C, H>;
+      constexpr size_t smem = (2 * (C / 2 * H + 4) + 128 * (C + 1) + 128 * H + C * (H + 2)) * 4;
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k<<<grid, 256, smem, st>>>(a, make_fastdiv((uint32_t)a.Lj));
+      return cudaGetLastError();
+    }
+  }
   const unsigned grid = (unsigned)((pb_warps(a) + 7) / 8);
   auto k = pair_bias_bwd_kernel<C, H>;
   constexpr size_t smem = 8 * (C * H + 2 * C) * 4;
