@@ -525,11 +525,12 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     const int64_t part_str[3] = {(int64_t)d->H * d->Lq * d->D,
                                  q_hfast ? d->D : (int64_t)d->Lq * d->D,
                                  q_hfast ? (int64_t)d->H * d->D : d->D};
-    if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str) ||
-        !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str) ||
-        !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str)
+    // 32-row boxes: each compute warp stores its own TMEM lane quarter
+    if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 32) ||
+        !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 32) ||
+        !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str, 32)
                   : make_x_map(&F.tm_dq, dqacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                               (int64_t)nk * d->B, d->H, d->Lq, d->D, part_str, 128,
+                               (int64_t)nk * d->B, d->H, d->Lq, d->D, part_str, 32,
                                std::min(dpad(d->D), 32))))
       return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for the output maps");
     evo::BwdFusedArgs& fa = F.args;

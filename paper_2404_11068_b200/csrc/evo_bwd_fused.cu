@@ -18,8 +18,8 @@
 //   MMA:      dV_b += Pᵀ·dA_j (A = Pᵀ from TMEM), dK_b += dSᵀ·Q_j;  after the 4 sub-tiles of a tile:
 //             dQ_part = dS·K_b (A = the tile's dSᵀ blocks read MN-major)
 // Drains: group 1 the previous tile's dQ part after its first sub-tile of a tile, group 0 dK/dV
-// at a new batch row, through swizzled staging tiles and TMA stores (direct per-thread global
-// stores of the rows measured ~10% slower).
+// at a new batch row, through swizzled staging tiles and per-warp TMA stores of 32-row slices
+// (direct per-thread global stores of the rows measured ~10% slower).
 // The issuer runs Sᵀ/dPᵀ ahead (one sub-tile pair), so before overwriting its Pᵀ slot a group
 // waits for dV/dK(j-2) (bar_mm).  The dSᵀ blocks are double-buffered per 128-query tile (buffer
 // T & 1): a group starting tile T waits only for tile T-2's dQ MMA, long done, instead of the
@@ -336,9 +336,13 @@ __global__ void __launch_bounds__(384, 1)
     // of the previous query tile (straight from TMEM to global memory, each thread its own row),
     // so the two groups share the drain work and group 0's dK/dV release (which gates the
     // gradient issuer) is not queued behind the dQ store.
+    // Each warp drains its own 32 rows (its TMEM lane quarter) into its slice of the staging tile
+    // and issues that slice's TMA store itself (32-row boxes): no group-wide barrier, no single
+    // issuing thread.
+    const uint32_t slice = (uint32_t)(qd * 32);
     auto drain_kv = [&](int bk, bool release_kv) {  // group 0
-      if (tid == 0) bulk_wait_group_read0();
-      named_bar_sync(2, 128);
+      if (lane == 0) bulk_wait_group_read0();  // this warp's previous stores left its slices
+      __syncwarp();
       uint32_t r[DP];
       tmem_ld_cols(tdK + lane_base, r);
       tmem_wait_ld();
@@ -352,10 +356,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       stage_bf16(s0 + C::oStV, r, 1.f);
       fence_proxy_async_smem();
-      named_bar_sync(2, 128);
-      if (tid == 0) {
-        tma_store_4d(&tm_dk, s0 + C::oStK, 0, k0, h, bk);
-        tma_store_4d(&tm_dv, s0 + C::oStV, 0, k0, h, bk);
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(&tm_dk, s0 + C::oStK + slice * kRbB, 0, k0 + (int)slice, h, bk);
+        tma_store_4d(&tm_dv, s0 + C::oStV + slice * kRbB, 0, k0 + (int)slice, h, bk);
         bulk_commit_group();
       }
     };
@@ -364,8 +368,8 @@ __global__ void __launch_bounds__(384, 1)
     auto drain_q = [&](int Tq) {
       mbar_wait(bar_dq + 8 * (Tq & 1), (Tq >> 1) & 1);
       tc_fence_after();
-      if (tid == 128) bulk_wait_group_read0();
-      named_bar_sync(3, 128);
+      if (lane == 0) bulk_wait_group_read0();
+      __syncwarp();
       uint32_t r[DP];
       tmem_ld_cols(tdQ + lane_base, r);
       tmem_wait_ld();
@@ -378,10 +382,12 @@ __global__ void __launch_bounds__(384, 1)
                        r[4 * i + 3]);
       }
       fence_proxy_async_smem();
-      named_bar_sync(3, 128);
-      if (tid == 128) {
+      __syncwarp();
+      if (lane == 0) {
         const int bq = b0 + Tq / nq;
-        tma_store_4d(&tm_dq, s0 + C::oStQ, 0, (Tq % nq) * 128, h, nk == 1 ? bq : kt * a.B + bq);
+        const uint32_t rb = nk == 1 ? kRbB : (uint32_t)(DP * 4);
+        tma_store_4d(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h,
+                     nk == 1 ? bq : kt * a.B + bq);
         bulk_commit_group();
       }
     };
@@ -526,11 +532,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(bar_dq + 8 * (Tl & 1), (Tl >> 1) & 1);
       tc_fence_after();
       drain_kv(b0 + nb - 1, false);
-      if (tid == 0) bulk_wait_group0();
     } else {
       drain_q(Tl);
-      if (tid == 128) bulk_wait_group0();
     }
+    if (lane == 0) bulk_wait_group0();
     if (BIAS) {  // partial[c][h][q][k0 + row]: this group's 32-query column blocks
       float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
       for (int cbk = g; cbk < Lq_pad / 32; cbk += 2) {
