@@ -6,7 +6,8 @@
 #include "../../paper_2404_11068_b200/csrc/evo_common.cuh"
 using namespace evo;
 
-// MODE 0: SS, 1: TS (A from TMEM).  NACC accumulators rotated (independent D) or 1 (chained D).
+// MODE 0: SS, 1: TS (A from TMEM), 2: SS with B MN-major, 3: SS with A and B MN-major (SW64,
+// the backward's dV/dK and dQ operand forms).  NACC accumulators rotated or 1 (chained D).
 template <int N, int MODE, int NACC>
 __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -23,11 +24,13 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) 
   tc_fence_after();
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
-    constexpr uint32_t idesc = make_idesc_bf16(128, N, 0, 0);
-    const uint64_t ad = make_sdesc(s0, 16, 512, kSw64), bd = make_sdesc(s0 + 65536, 16, 512, kSw64);
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, MODE == 3 ? 1 : 0, MODE >= 2 ? 1 : 0);
+    const uint64_t ad = MODE == 3 ? make_sdesc(s0, 8192, 512, kSw64) : make_sdesc(s0, 16, 512, kSw64);
+    const uint64_t bd = MODE >= 2 ? make_sdesc(s0 + 65536, 16384, 512, kSw64)
+                                  : make_sdesc(s0 + 65536, 16, 512, kSw64);
     // latency: one MMA, commit, wait
     unsigned long long t0 = clock64();
-    if (MODE == 0) umma_bf16(tm, ad, bd, idesc, 0);
+    if (MODE != 1) umma_bf16(tm, ad, bd, idesc, 0);
     else umma_bf16_ts(tm, tm + 256, bd, idesc, 0);
     umma_commit(smem_u32(&bar));
     mbar_wait(smem_u32(&bar), 0);
@@ -35,7 +38,7 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) 
     // throughput: n_mma back to back
     for (int i = 0; i < n_mma; ++i) {
       const uint32_t d = tm + (uint32_t)((i % NACC) * N) % 256;
-      if (MODE == 0) umma_bf16(d, ad, bd, idesc, 1);
+      if (MODE != 1) umma_bf16(d, ad, bd, idesc, 1);
       else umma_bf16_ts(d, tm + 256, bd, idesc, 1);
     }
     umma_commit(smem_u32(&bar));
@@ -62,8 +65,9 @@ void run(unsigned long long* d) {
   unsigned long long h[2];
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
   const double per = (double)h[1] / n;
-  printf("N=%3d %s nacc=%d: latency %5llu cyc, %6.1f cyc/MMA (K=16) -> %6.0f flop/clk/SM (%.0f%% of 8192)\n",
-         N, MODE ? "TS" : "SS", NACC, h[0], per, 2.0 * 128 * N * 16 / per,
+  const char* mn[4] = {"SS", "TS", "SS-Bmn", "SS-ABmn"};
+  printf("N=%3d %-7s nacc=%d: latency %5llu cyc, %6.1f cyc/MMA (K=16) -> %6.0f flop/clk/SM (%.0f%% of 8192)\n",
+         N, mn[MODE], NACC, h[0], per, 2.0 * 128 * N * 16 / per,
          100.0 * 2.0 * 128 * N * 16 / per / 8192);
 }
 
@@ -80,5 +84,10 @@ int main() {
   run<128, 0, 2>(d);
   run<256, 0, 1>(d);
   run<16, 0, 4>(d);
+  run<32, 2, 1>(d);
+  run<32, 2, 4>(d);
+  run<32, 3, 1>(d);
+  run<32, 3, 4>(d);
+  run<64, 2, 1>(d);
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
