@@ -125,3 +125,13 @@ def test_bf16_parity_many_batch_rows(B, H, L, bias):
     errs, _, _ = run_case(B, H, L, L, 32, seed=3, bias=bias, gate=True, mask="prefix",
                           mask_t=False, layout="blhd")
     _assert(errs, torch.bfloat16, f"B={B} H={H} L={L} bias={bias}")
+
+
+@pytest.mark.parametrize("B,H,L", [(40, 2, 256), (200, 1, 128)])
+def test_bf16_parity_end_node_many_chunks(B, H, L):
+    """End-node view (q-contiguous bias, transposed mask) with many batch chunks: the transposed
+    dbias reduce over more partials than one load round holds (16), and the per-warp drains of
+    the fused backward on the [J, I] storage."""
+    errs, _, _ = run_case(B, H, L, L, 32, seed=7, bias="shared", bias_t=True, gate=True,
+                          mask="prefix", mask_t=True, layout="lbhd")
+    _assert(errs, torch.bfloat16, f"end-node B={B} H={H} L={L}")
