@@ -114,6 +114,9 @@ EVO_DEV void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes, uint3
       : "memory");
 }
 // make generic-proxy shared-memory writes visible to the async proxy (tensor core / TMA)
+EVO_DEV void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 EVO_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
