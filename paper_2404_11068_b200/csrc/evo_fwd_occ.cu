@@ -121,10 +121,12 @@ __global__ void __launch_bounds__(128, 4)
       if (kk < a.Lk) keep_pre[x] = a.mask ? (uint32_t)a.mask[(int64_t)b * a.mask_s0 + (int64_t)kk * a.mask_s1] : 1u;
     }
   }
-  // The gate row is read in the epilogue (an L2 prefetch issued here hides its latency behind
-  // the key loop) instead of with the Q row into TMEM: −5% forward time (51.7 -> 49.1 us per
-  // call, bench mean over the four modules).  EVO_FWD_FLAGS bit 1 restores the prologue load.
-  const bool late_g = (a.flags & 2) == 0;
+  // With more than two key chunks the gate row is read in the epilogue (an L2 prefetch issued
+  // here hides its latency behind the key loop) instead of with the Q row into TMEM: L = 256
+  // forward 54.2 / 55.3 / 63.5 -> 51.2 / 51.3 / 57.3 us (row / start / end).  Two chunks are
+  // too short to hide it (MSA column, L = 128: 36.9 early vs 38.9 late), so the gate rides with
+  // Q there.  EVO_FWD_FLAGS bit 1 forces the prologue load.
+  const bool late_g = nc > 2 && (a.flags & 2) == 0;
   {
     uint32_t qrow[DP / 2], gpk[DP / 2];
     const __nv_bfloat16* qp = qptr + (int64_t)b * q_sb + (int64_t)h * q_sh + (int64_t)q * q_sl;
