@@ -293,25 +293,36 @@ __global__ void __launch_bounds__(384, 1)
             }
           }
         }
-      } else {  // q-contiguous rows: thread per key row, 8 queries per 16-B load
-        for (int r = tid; r < 128; r += 256) {
-          const __nv_bfloat16* src = bp + (int64_t)(k0 + r) * a.b_sk;
-          const bool kv = k0 + r < a.Lk;
-          for (int q8 = 0; q8 < Lq_pad / 8; ++q8) {
-            uint4 u = make_uint4(0, 0, 0, 0);
+      } else {
+        // q-contiguous rows (end-node view): two threads per key row, each taking half of the
+        // 8-query chunks with 8 independent 16-B loads in flight (one thread walking a row
+        // chunk by chunk serialised a load latency per chunk in front of the first sub-tile)
+        const int r = tid & 127, half = tid >> 7;
+        const __nv_bfloat16* src = bp + (int64_t)(k0 + r) * a.b_sk;
+        const bool kv = k0 + r < a.Lk;
+        const int per = Lq_pad / 16;  // chunks per half: a multiple of 8
+        for (int q8b = half * per; q8b < (half + 1) * per; q8b += 8) {
+          uint4 u[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const int q8 = q8b + x;
+            u[x] = make_uint4(0, 0, 0, 0);
             if (kv && q8 * 8 < a.Lq) {
               if (q8 * 8 + 7 < a.Lq) {
-                u = *reinterpret_cast<const uint4*>(src + q8 * 8);
+                u[x] = *reinterpret_cast<const uint4*>(src + q8 * 8);
               } else {
                 uint16_t e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (int e = 0; e < 8; ++e)
                   if (q8 * 8 + e < a.Lq) e8[e] = __bfloat16_as_ushort(src[q8 * 8 + e]);
-                u = make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16), e8[4] | (e8[5] << 16),
-                               e8[6] | (e8[7] << 16));
+                u[x] = make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16), e8[4] | (e8[5] << 16),
+                                  e8[6] | (e8[7] << 16));
               }
             }
-            st_shared_v4(sBias + r * RB + (((uint32_t)q8 ^ (r & 7)) << 4), u.x, u.y, u.z, u.w);
           }
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+            st_shared_v4(sBias + r * RB + (((uint32_t)(q8b + x) ^ (r & 7)) << 4), u[x].x, u[x].y, u[x].z,
+                         u[x].w);
         }
       }
       named_bar_sync(1, 256);
