@@ -551,6 +551,10 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.p_sb = part_str[0]; fa.p_sh = part_str[1]; fa.p_sl = part_str[2];
     static const int bwd_flags = getenv("EVO_BWD_FLAGS") ? atoi(getenv("EVO_BWD_FLAGS")) : 0;
     fa.flags = bwd_flags;
+    fa.bmode = bm;
+    memset(&F.tm_b, 0, sizeof(F.tm_b));
+    if (bm && !make_bias_map(&F.tm_b, d, bias, bm == 1 ? 256 : 128))
+      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for the fused backward's bias map");
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
     static const bool dbg_timing_b = getenv("EVO_DEBUG_TIMING") != nullptr;
     fa.dbg = dbg_timing_b ? evo::fwd_debug_ptr() : nullptr;

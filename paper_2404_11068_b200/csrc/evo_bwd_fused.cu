@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(384, 1)
     bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_da,
                      const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
-                     const __grid_constant__ CUtensorMap tm_dv, const BwdFusedArgs a) {
+                     const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_b,
+                     const BwdFusedArgs a) {
   using C = FusedCfg<DP, BIAS>;
   static_assert(DP == 16 || DP == 32, "fused backward: head dim pad 16 or 32");
   constexpr uint32_t kSw = DP == 32 ? kSw64 : kSw32;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t bar_ps = smem_u32(&bars[12]);      // +8            Pᵀ, dSᵀ in smem (4 warps)
   const uint32_t bar_dq = smem_u32(&bars[18]);      // +8: dSᵀ buffer 1   dQ MMA of a tile done
   const uint32_t bar_dkvfree = smem_u32(&bars[15]); // group 0 pulled a finished dK/dV (4 warps)
+  const uint32_t bar_bias = smem_u32(&bars[14]);    // the bias tiles of the prologue landed (TMA)
   const uint32_t bar_mm = smem_u32(&bars[16]);      // +8: group 1   dV/dK of its sub-tile done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[20]);
 
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(bar_dq, 1);
     mbar_init(bar_dq + 8, 1);
     mbar_init(bar_dkvfree, 4);
+    mbar_init(bar_bias, 1);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -246,83 +249,43 @@ __global__ void __launch_bounds__(384, 1)
     const int g = w >> 2, qd = w & 3;
     const int row = qd * 32 + lane;  // key row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
-    const uint32_t RB = (uint32_t)Lq_pad * 2;  // resident biasᵀ row bytes
     const uint32_t sBias = s0 + C::oBias;
     if (BIAS) {
-      // biasᵀ[k][q] = bias[h, q, k0 + k] for q < Lq, k0 + k < Lk; 0 elsewhere (padding must be
-      // finite: it meets zero P/dA rows in the MMAs)
-      const __nv_bfloat16* bp = a.bias + (int64_t)h * a.b_sh;
-      if (a.b_sk == 1) {
-        // k-contiguous rows: a lane loads 8 keys of one query (16 B) and scatters them down the
-        // 8 key rows of its column; the 32 lanes of a warp take 32 consecutive queries, so each
-        // 2-byte store instruction hits 4 swizzled chunks x 8 lanes = no bank conflict
-        const int nunits = (Lq_pad / 32) * 16;  // (32-query block, 8-key group) units
-        for (int u0 = w; u0 < nunits; u0 += 8 * 4) {
-          uint4 v[4];
-          int qq[4], kk8[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {  // 4 independent loads in flight per lane
-            const int u = u0 + x * 8;
-            qq[x] = (u / 16) * 32 + lane;
-            kk8[x] = (u % 16) * 8;
-            v[x] = make_uint4(0, 0, 0, 0);
-            if (u < nunits && qq[x] < a.Lq) {
-              const __nv_bfloat16* src = bp + (int64_t)qq[x] * a.b_sq + k0 + kk8[x];
-              if (k0 + kk8[x] + 7 < a.Lk) {
-                v[x] = *reinterpret_cast<const uint4*>(src);
-              } else {
-                uint16_t e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int e = 0; e < 8; ++e)
-                  if (k0 + kk8[x] + e < a.Lk) e8[e] = __bfloat16_as_ushort(src[e]);
-                v[x] = make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16),
-                                  e8[4] | (e8[5] << 16), e8[6] | (e8[7] << 16));
-              }
-            }
-          }
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            if (u0 + x * 8 >= nunits) break;
-            const uint32_t q = (uint32_t)qq[x];
-            const uint32_t w4[4] = {v[x].x, v[x].y, v[x].z, v[x].w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const uint32_t r = (uint32_t)kk8[x] + e;
-              const uint16_t val = (uint16_t)(e & 1 ? w4[e >> 1] >> 16 : w4[e >> 1] & 0xffff);
-              const uint32_t addr = sBias + r * RB + (((q >> 3) ^ (r & 7)) << 4) + (q & 7) * 2;
-              asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(val) : "memory");
-            }
-          }
+      // biasᵀ[k][q] = bias[h, q, k0 + k] for q < Lq, k0 + k < Lk; 0 elsewhere (TMA zero fill:
+      // padding must be finite, it meets zero P/dA rows in the MMAs).  Resident layout: Lq_pad / 64
+      // segments of [128 k][64 q] with 128-B rows, 16-B chunks XOR-swizzled by k & 7 (the TMA
+      // 128-B swizzle), so a q-contiguous (end-node) bias lands there straight from TMA, and a
+      // k-contiguous one is staged [q][64 k] x 2 in the (not yet used) dSᵀ buffers and transposed
+      // 8 x 8 blocks at a time by ldmatrix + stmatrix.trans (conflict-free both ways).
+      if (tid == 0) {
+        if (a.bmode == 2) {
+          mbar_arrive_expect_tx(bar_bias, (uint32_t)(Lq_pad / 64) * 16384u);
+          for (int sg = 0; sg < Lq_pad / 64; ++sg)
+            tma_load_4d(sBias + sg * 16384, &tm_b, bar_bias, sg * 64, k0, h, 0);
+        } else {
+          mbar_arrive_expect_tx(bar_bias, 65536u);
+          tma_load_4d(s0 + C::oDS, &tm_b, bar_bias, k0, 0, h, 0);
+          tma_load_4d(s0 + C::oDS + 32768, &tm_b, bar_bias, k0 + 64, 0, h, 0);
         }
-      } else {
-        // q-contiguous rows (end-node view): two threads per key row, each taking half of the
-        // 8-query chunks with 8 independent 16-B loads in flight (one thread walking a row
-        // chunk by chunk serialised a load latency per chunk in front of the first sub-tile)
-        const int r = tid & 127, half = tid >> 7;
-        const __nv_bfloat16* src = bp + (int64_t)(k0 + r) * a.b_sk;
-        const bool kv = k0 + r < a.Lk;
-        const int per = Lq_pad / 16;  // chunks per half: a multiple of 8
-        for (int q8b = half * per; q8b < (half + 1) * per; q8b += 8) {
-          uint4 u[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const int q8 = q8b + x;
-            u[x] = make_uint4(0, 0, 0, 0);
-            if (kv && q8 * 8 < a.Lq) {
-              if (q8 * 8 + 7 < a.Lq) {
-                u[x] = *reinterpret_cast<const uint4*>(src + q8 * 8);
-              } else {
-                uint16_t e8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int e = 0; e < 8; ++e)
-                  if (q8 * 8 + e < a.Lq) e8[e] = __bfloat16_as_ushort(src[q8 * 8 + e]);
-                u[x] = make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16), e8[4] | (e8[5] << 16),
-                                  e8[6] | (e8[7] << 16));
-              }
-            }
-          }
-#pragma unroll
-          for (int x = 0; x < 8; ++x)
-            st_shared_v4(sBias + r * RB + (((uint32_t)(q8b + x) ^ (r & 7)) << 4), u[x].x, u[x].y, u[x].z,
-                         u[x].w);
+      }
+      mbar_wait(bar_bias, 0);
+      if (a.bmode != 2) {
+        const int mi = lane >> 3, ri = lane & 7;
+        for (int gi = w; gi < (Lq_pad / 8) * 4; gi += 8) {  // x4 group: q block q8, k blocks 4 kk..4 kk+3
+          const int q8 = gi >> 2, k8 = (gi & 3) * 4 + mi;
+          const uint32_t q = (uint32_t)(q8 * 8 + ri);
+          const uint32_t src = s0 + C::oDS + (uint32_t)(k8 >> 3) * 32768u + q * 128u +
+                               ((((uint32_t)k8 & 7u) ^ (q & 7u)) << 4);
+          uint32_t r0, r1, r2, r3;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                       : "r"(src));
+          const uint32_t k = (uint32_t)(k8 * 8 + ri);
+          const uint32_t dst = sBias + (uint32_t)(q8 >> 3) * 16384u + k * 128u +
+                               ((((uint32_t)q8 & 7u) ^ (k & 7u)) << 4);
+          asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                       "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                       : "memory");
         }
       }
       named_bar_sync(1, 256);
@@ -333,7 +296,6 @@ __global__ void __launch_bounds__(384, 1)
     const int kglob = k0 + row;
     // ---- drains (group 0): TMEM rows -> swizzled staging tiles -> one thread's TMA stores
     constexpr uint32_t kRbB = DP * 2;  // bf16 staging row bytes (= the x-map swizzle span)
-    constexpr uint32_t kRbF = DP * 4;  // fp32 staging row bytes
     auto stage_bf16 = [&](uint32_t base, const uint32_t (&r)[DP], float mul) {
 #pragma unroll
       for (int i = 0; i < DP / 8; ++i)
@@ -459,7 +421,8 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t nd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
         uint32_t bu[4] = {0, 0, 0, 0};
         if (BIAS) {
-          const uint4 bv = ld_shared_v4(sBias + row * RB + (((uint32_t)(qcol >> 3) + gq) ^ (row & 7)) * 16);
+          const uint32_t cq = (uint32_t)(qcol >> 3) + gq;  // 8-query chunk
+          const uint4 bv = ld_shared_v4(sBias + (cq >> 3) * 16384u + row * 128u + (((cq & 7u) ^ (row & 7u)) << 4));
           bu[0] = bv.x; bu[1] = bv.y; bu[2] = bv.z; bu[3] = bv.w;
         }
 #pragma unroll
@@ -574,7 +537,7 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
   kern<<<(unsigned)grid, 384, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk, L.tm_dv,
-                                          L.args);
+                                          L.tm_b, L.args);
   return cudaGetLastError();
 }
 

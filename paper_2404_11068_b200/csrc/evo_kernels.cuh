@@ -157,9 +157,10 @@ struct BwdFusedArgs {
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
   unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
   int flags;  // experiment switches (EVO_BWD_FLAGS), 0 in production
+  int bmode;  // bias: 1 k-contiguous (tm_b box [256 q][64 k]), 2 q-contiguous (box [128 k][64 q])
 };
 struct BwdFusedLaunch {
-  CUtensorMap tm_q, tm_k, tm_v, tm_da;
+  CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
   CUtensorMap tm_dq, tm_dk, tm_dv;  // output maps (dq: bf16 over dq, or fp32 over the dQ parts)
   BwdFusedArgs args;
 };
