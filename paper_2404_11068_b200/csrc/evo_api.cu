@@ -475,6 +475,20 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   const int64_t da_str[3] = {(int64_t)d->H * d->Lq * d->D, o_hfast ? d->D : (int64_t)d->Lq * d->D,
                              o_hfast ? (int64_t)d->H * d->D : d->D};
   pa.a_sb = da_str[0]; pa.a_sh = da_str[1]; pa.a_sl = da_str[2];
+  // dQ over several key tiles: the fused backward reduce-adds (TMA .add, performed at L2) every
+  // key tile's fp32 dQ into ONE accumulator that the vectorised bwd_pre zero-fills on its way —
+  // one fp32 part read by dq_convert instead of one per key tile
+  const int64_t pre_vec = (int64_t)d->B * d->H * ((d->Lq + 127) / 128 * 128) * (d->D / 8);
+  const bool dq_red = W.fused && nk > 1 && d->dtype != EVO_F32 && d->D % 8 == 0 &&
+                      pre_vec < ((int64_t)1 << 31) &&  // the conditions of bwd_pre's vector path
+                      !getenv("EVO_BWD_PRE_OLD") && !getenv("EVO_DQ_PARTS");
+  if (dq_red) {  // bwd_pre zero-fills the accumulator in the layout of the dQ parts
+    const bool qh = d->q_str[1] < d->q_str[2];
+    pa.zacc = reinterpret_cast<float*>(ws + W.dqacc);
+    pa.z_sb = (int64_t)d->H * d->Lq * d->D;
+    pa.z_sh = qh ? d->D : (int64_t)d->Lq * d->D;
+    pa.z_sl = qh ? (int64_t)d->H * d->D : d->D;
+  }
   if ((e = traced(st, "bwd_pre", [&] { return evo::launch_bwd_pre(pa, d->dtype == EVO_F32, st); })) != cudaSuccess) return cuda_fail(e, "bwd_pre");
   ++nl;
   // dA operand: workspace [B,H,Lq,D] contiguous, or dout itself when there is no gate
@@ -551,6 +565,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.p_sb = part_str[0]; fa.p_sh = part_str[1]; fa.p_sl = part_str[2];
     static const int bwd_flags = getenv("EVO_BWD_FLAGS") ? atoi(getenv("EVO_BWD_FLAGS")) : 0;
     fa.flags = bwd_flags;
+    fa.dq_reduce = dq_red ? 1 : 0;
     fa.bmode = bm;
     memset(&F.tm_b, 0, sizeof(F.tm_b));
     if (bm && !make_bias_map(&F.tm_b, d, bias, bm == 1 ? 256 : 128))
@@ -580,7 +595,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     if (dqacc) {
       evo::ConvertArgs ca{};
       ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
-      ca.nparts = nk; ca.part_stride = (int64_t)d->B * d->H * d->Lq * d->D;
+      ca.nparts = fa.dq_reduce ? 1 : nk; ca.part_stride = (int64_t)d->B * d->H * d->Lq * d->D;
       ca.p_sb = part_str[0]; ca.p_sh = part_str[1]; ca.p_sl = part_str[2];
       ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
       if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");

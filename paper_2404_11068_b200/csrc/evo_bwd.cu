@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += 2 * stride) {  // block-uniform trip
     uint4 ov[2], dv[2], gv[2];
     float l[2];
-    int64_t orow[2], grow[2], arow[2], vrow[2];
+    int64_t orow[2], grow[2], arow[2], vrow[2], zrow[2];
     bool ok[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
       grow[u] = b * a.g_sb + h * a.g_sh + (int64_t)q * a.g_sl + c * 8;
       arow[u] = b * a.a_sb + h * a.a_sh + (int64_t)q * a.a_sl + c * 8;
       vrow[u] = (b * H + h) * Lq_pad + q;
+      zrow[u] = b * a.z_sb + h * a.z_sh + (int64_t)q * a.z_sl + c * 8;
       ov[u] = dv[u] = gv[u] = make_uint4(0, 0, 0, 0);
       l[u] = 0.f;
       if (ok[u]) {
@@ -232,6 +233,11 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
 #pragma unroll
       for (int m = 1; m < NCH; m <<= 1) Dq += __shfl_xor_sync(0xffffffffu, Dq, m);
       if (!ok[u]) continue;
+      if (a.zacc) {
+        float4* z = reinterpret_cast<float4*>(a.zacc + zrow[u]);
+        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       if (g_p) {
         *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow[u]) =
             make_uint4(pa[0], pa[1], pa[2], pa[3]);
@@ -259,6 +265,8 @@ cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   if (items == 0) return cudaSuccess;
   const int64_t nvec = (int64_t)a.B * a.H * Lq_pad * (a.D / 8);
   static const bool old_pre = getenv("EVO_BWD_PRE_OLD") != nullptr;  // A/B switch
+  // only the vector path zero-fills a dQ accumulator; the caller selects it whenever it asks
+  if (a.zacc && !(!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre)) return cudaErrorInvalidValue;
   if (!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre) {
     BwdPreArgs v = a;
     v.fd_H = make_fastdiv((uint32_t)a.H);

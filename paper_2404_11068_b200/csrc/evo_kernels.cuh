@@ -83,6 +83,8 @@ struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
   void* dA;      // dO·sigmoid(g) (NULL when no gate), element strides below, d unit-stride
   int64_t a_sb, a_sh, a_sl;
   int negate;    // store -lse2 and -D (the fused backward's operand form)
+  float* zacc;   // optional fp32 [B,H,Lq,D] accumulator zeroed here (strides below), else NULL
+  int64_t z_sb, z_sh, z_sl;
   FastDiv fd_H, fd_Lq;  // filled by launch_bwd_pre
 };
 cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st);
@@ -157,6 +159,7 @@ struct BwdFusedArgs {
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
   unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
   int flags;  // experiment switches (EVO_BWD_FLAGS), 0 in production
+  int dq_reduce;  // 1: every key tile reduce-adds its dQ into ONE fp32 accumulator (zeroed by bwd_pre)
   int bmode;  // bias: 1 k-contiguous (tm_b box [256 q][64 k]), 2 q-contiguous (box [128 k][64 q])
 };
 struct BwdFusedLaunch {
