@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
       if (!ok[u]) continue;
       if (a.zacc) {
         float4* z = reinterpret_cast<float4*>(a.zacc + zrow[u]);
-        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint64_t pol = l2_policy_evict_last();  // keep the zeroed lines in L2 for bwd_fused's adds
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z), "f"(0.f), "l"(pol) : "memory");
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z + 1), "f"(0.f), "l"(pol) : "memory");
       }
       if (g_p) {
         *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow[u]) =

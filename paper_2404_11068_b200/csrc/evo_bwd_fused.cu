@@ -359,8 +359,10 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) {
         const int bq = b0 + Tq / nq;
         const uint32_t rb = nk == 1 ? kRbB : (uint32_t)(DP * 4);
-        if (nk > 1 && a.dq_reduce)  // TMA .add at L2 into one fp32 accumulator (bwd_pre zeroed it)
-          tma_reduce_add_4d(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h, bq);
+        if (nk > 1 && a.dq_reduce)  // TMA .add at L2 into one fp32 accumulator (bwd_pre zeroed it),
+          // evict_last so the lines stay in L2 for the other key tiles' adds and for dq_convert
+          tma_reduce_add_4d_hint(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h, bq,
+                                 l2_policy_evict_last());
         else
           tma_store_4d(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h,
                        nk == 1 ? bq : kt * a.B + bq);

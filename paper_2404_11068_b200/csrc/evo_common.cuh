@@ -101,13 +101,20 @@ EVO_DEV void tma_store_4d(const void* tmap, uint32_t smem_src, int c0, int c1, i
       "r"(smem_src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-// 4-D tiled reduce-add shared -> global (f32 add performed at L2; bulk-group completion)
-EVO_DEV void tma_reduce_add_4d(const void* tmap, uint32_t smem_src, int c0, int c1, int c2, int c3) {
+// 4-D tiled reduce-add shared -> global (f32 add performed at L2; bulk-group completion) with an
+// L2 cache policy (e.g. evict_last so the accumulator stays for its reader)
+EVO_DEV void tma_reduce_add_4d_hint(const void* tmap, uint32_t smem_src, int c0, int c1, int c2, int c3,
+                                    uint64_t pol) {
   asm volatile(
-      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(tmap)),
-      "r"(smem_src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group.L2::cache_hint"
+      " [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
       : "memory");
+}
+EVO_DEV uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 EVO_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the issuing thread's bulk groups have finished READING shared memory
