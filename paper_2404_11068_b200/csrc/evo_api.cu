@@ -22,8 +22,26 @@ void set_error_detail(const char* msg) { g_detail = msg; }
 }  // namespace evo
 namespace {
 thread_local int g_launches = 0;
-constexpr int kNumSMs = 148;  // B200; fixes the dbias batch chunking (workspace is a pure
-                              // function of the descriptor)
+// SM count of the current device: fixes the batch chunking of the dbias partials (one CTA per SM
+// in the fused backward), so the workspace is a function of the descriptor and the device.
+// Queried once per device (148 on B200; no device -> 148, so the CPU-side size queries agree).
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    (void)cudaGetLastError();
+    return 148;
+  }
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      (void)cudaGetLastError();
+      n = 148;
+    }
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
 
 evo_status_t fail(evo_status_t s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 evo_status_t fail(evo_status_t s, const char* fmt, ...) {
@@ -139,13 +157,22 @@ struct WsLayout {
   int nchunks = 1, chunk = 1;
   bool fused = false;
 };
-// Single-pass backward (evo_bwd_fused.cu) for bf16 with a shared bias or none and Lq <= 256;
-// EVO_BWD_IMPL=split forces the two-pass kernels (A/B experiments).
+// Single-pass backward (evo_bwd_fused.cu) for bf16 with a shared bias or none and Lq <= 256
 bool use_fused_bwd(const evo_attn_desc_t* d) {
-  static const bool split = getenv("EVO_BWD_IMPL") && !strcmp(getenv("EVO_BWD_IMPL"), "split");
-  if (split || d->dtype != EVO_BF16 || d->bias_kind == EVO_BIAS_PER_BATCH) return false;
+  if (d->dtype != EVO_BF16 || d->bias_kind == EVO_BIAS_PER_BATCH) return false;
   const int Lq_pad = ((d->Lq + 127) / 128) * 128;
   return evo::bwd_fused_supported(dpad(d->D), Lq_pad, d->bias_kind != EVO_BIAS_NONE);
+}
+// dQ over several key tiles.  Determinism (bitwise-repeatable backward): with
+// exactly two key tiles both reduce-add (TMA .add at L2) into ONE fp32 accumulator that bwd_pre
+// zero-fills, and 0 + a + b = 0 + b + a exactly, so the order of the two adds cannot change a
+// bit; with three or more key tiles fp32 addition is not associative, so every key tile stores
+// its own fp32 part and dq_convert sums the parts in key-tile order 0, 1, ..., nk-1.
+bool use_dq_reduce(const evo_attn_desc_t* d) {
+  const int64_t nk = (d->Lk + 127) / 128;
+  const int64_t pre_vec = d->B * d->H * ((d->Lq + 127) / 128 * 128) * (d->D / 8);
+  return use_fused_bwd(d) && nk == 2 && d->D % 8 == 0 &&
+         pre_vec < ((int64_t)1 << 31);  // the conditions of bwd_pre's vectorised path
 }
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -159,10 +186,9 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
   w.dvec = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   if (d->has_gate) { w.da = off; off = al256(off + (size_t)rows * d->Lq * d->D * esize(d)); }
   if (d->dtype == EVO_BF16 && nk > 1) {
-    // fused: one fp32 dQ part per key tile (plain stores); split: one atomic sum
-    const bool fused = use_fused_bwd(d);
+    // one fp32 accumulator (nk == 2, reduce-add) or one fp32 part per key tile (use_dq_reduce)
     w.dqacc = off;
-    const int64_t parts = fused ? nk : 1;
+    const int64_t parts = use_dq_reduce(d) ? 1 : nk;
     off = al256(off + (size_t)parts * rows * d->Lq * d->D * 4);
   }
   w.fused = use_fused_bwd(d);
@@ -170,11 +196,11 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
     int64_t nch, chunk;
     if (w.fused) {
       int ch = 1;
-      nch = evo::bwd_fused_nchunks((int)d->B, d->H, (int)nk, kNumSMs, &ch);
+      nch = evo::bwd_fused_nchunks((int)d->B, d->H, (int)nk, num_sms(), &ch);
       chunk = ch;
     } else {
       const int64_t tiles = (int64_t)d->H * nq * nk;
-      nch = (2 * kNumSMs + tiles - 1) / std::max<int64_t>(tiles, 1);
+      nch = (2 * num_sms() + tiles - 1) / std::max<int64_t>(tiles, 1);
       nch = std::max<int64_t>(1, std::min<int64_t>(nch, d->B));
       chunk = (d->B + nch - 1) / nch;
       nch = (d->B + chunk - 1) / chunk;
@@ -372,17 +398,15 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
     g_launches = 1;
     return e == cudaSuccess ? EVO_OK : cuda_fail(e, "fwd_f32");
   }
-  evo::FwdLaunch L;
-  memset(&L, 0, sizeof(L));
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  if (!make_x_map(&L.tm_q, q, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str) ||
-      !make_x_map(&L.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str) ||
-      !make_x_map(&L.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str))
-    return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for q/k/v");
   const int bm = bias_mode(d);
-  if (bm && !make_bias_map(&L.tm_b, d, bias))
-    return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
-  evo::FwdArgs& a = L.args;
+  evo::FwdOccLaunch O;
+  memset(&O, 0, sizeof(O));
+  if (!make_x_map(&O.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||
+      !make_x_map(&O.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 64) ||
+      (bm && !make_bias_map(&O.tm_b, d, bias, bm == 1 ? 128 : 64)))
+    return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for k/v/bias");
+  evo::FwdArgs& a = O.args;
   a.B = (int)d->B; a.H = d->H; a.Lq = d->Lq; a.Lk = d->Lk; a.D = d->D;
   a.scale = d->scale;
   a.scale_log2 = d->scale * evo::kLog2e;
@@ -391,41 +415,9 @@ evo_status_t evo_attn_fwd(const evo_attn_desc_t* d, const void* q, const void* k
   a.g = (const __nv_bfloat16*)g; a.g_sb = d->g_str[0]; a.g_sh = d->g_str[1]; a.g_sl = d->g_str[2];
   a.o = (__nv_bfloat16*)o; a.o_sb = d->o_str[0]; a.o_sh = d->o_str[1]; a.o_sl = d->o_str[2];
   a.lse = lse;
-  static const bool dbg_timing = getenv("EVO_DEBUG_TIMING") != nullptr;
-  a.dbg = dbg_timing ? evo::fwd_debug_ptr() : nullptr;
-  static const int fwd_flags = getenv("EVO_FWD_FLAGS") ? atoi(getenv("EVO_FWD_FLAGS")) : 0;
-  a.flags = fwd_flags;
-  // kernel variant (A/B experiments only): "occ" (default), "ws", "v1"
-  static const char* impl = getenv("EVO_FWD_IMPL") ? getenv("EVO_FWD_IMPL") : "occ";
-  cudaError_t e;
-  if (!strcmp(impl, "pp") && dpad(d->D) <= 32) {
-    evo::FwdPpLaunch P;
-    memset(&P, 0, sizeof(P));
-    if (!make_x_map(&P.tm_q, q, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str) ||
-        (g && !make_x_map(&P.tm_g, g, dt, 2, d->B, d->H, d->Lq, d->D, d->g_str)) ||
-        !make_x_map(&P.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||
-        !make_x_map(&P.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 64) ||
-        (bm && !make_bias_map(&P.tm_b, d, bias, bm == 1 ? 128 : 64)))
-      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed (pp)");
-    P.args = a;
-    e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_pp_bf16(P, dpad(d->D), bm, st); });
-  } else if (!strcmp(impl, "occ") || !strcmp(impl, "pp")) {
-    evo::FwdOccLaunch O;
-    memset(&O, 0, sizeof(O));
-    if (!make_x_map(&O.tm_k, k, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 64) ||
-        !make_x_map(&O.tm_v, v, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 64) ||
-        (bm && !make_bias_map(&O.tm_b, d, bias, bm == 1 ? 128 : 64)))
-      return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed (occ)");
-    O.args = a;
-    O.q = (const __nv_bfloat16*)q;
-    O.q_sb = d->q_str[0]; O.q_sh = d->q_str[1]; O.q_sl = d->q_str[2];
-    e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_occ_bf16(O, dpad(d->D), bm, st); });
-  } else {
-    e = traced(st, "fwd_bf16", [&] {
-      return !strcmp(impl, "v1") ? evo::launch_fwd_bf16(L, dpad(d->D), bm, st)
-                                 : evo::launch_fwd_ws_bf16(L, dpad(d->D), bm, st);
-    });
-  }
+  O.q = (const __nv_bfloat16*)q;
+  O.q_sb = d->q_str[0]; O.q_sh = d->q_str[1]; O.q_sl = d->q_str[2];
+  cudaError_t e = traced(st, "fwd_bf16", [&] { return evo::launch_fwd_occ_bf16(O, dpad(d->D), bm, st); });
   g_launches = 1;
   return e == cudaSuccess ? EVO_OK : cuda_fail(e, "fwd_bf16");
 }
@@ -475,13 +467,10 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   const int64_t da_str[3] = {(int64_t)d->H * d->Lq * d->D, o_hfast ? d->D : (int64_t)d->Lq * d->D,
                              o_hfast ? (int64_t)d->H * d->D : d->D};
   pa.a_sb = da_str[0]; pa.a_sh = da_str[1]; pa.a_sl = da_str[2];
-  // dQ over several key tiles: the fused backward reduce-adds (TMA .add, performed at L2) every
-  // key tile's fp32 dQ into ONE accumulator that the vectorised bwd_pre zero-fills on its way —
-  // one fp32 part read by dq_convert instead of one per key tile
-  const int64_t pre_vec = (int64_t)d->B * d->H * ((d->Lq + 127) / 128 * 128) * (d->D / 8);
-  const bool dq_red = W.fused && nk > 1 && d->dtype != EVO_F32 && d->D % 8 == 0 &&
-                      pre_vec < ((int64_t)1 << 31) &&  // the conditions of bwd_pre's vector path
-                      !getenv("EVO_BWD_PRE_OLD") && !getenv("EVO_DQ_PARTS");
+  // dQ over two key tiles: the fused backward reduce-adds (TMA .add, performed at L2) both key
+  // tiles' fp32 dQ into ONE accumulator that the vectorised bwd_pre zero-fills on its way — one
+  // fp32 part read by dq_convert instead of two; see use_dq_reduce for determinism
+  const bool dq_red = use_dq_reduce(d);
   if (dq_red) {  // bwd_pre zero-fills the accumulator in the layout of the dQ parts
     const bool qh = d->q_str[1] < d->q_str[2];
     pa.zacc = reinterpret_cast<float*>(ws + W.dqacc);
@@ -526,10 +515,6 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (bm && !make_bias_map(&tb, d, bias)) return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
 
   float* dqacc = nk > 1 ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
-  if (dqacc && !W.fused) {
-    if ((e = cudaMemsetAsync(dqacc, 0, (size_t)d->B * d->H * d->Lq * d->D * 4, st)) != cudaSuccess)
-      return cuda_fail(e, "memset dq_acc");
-  }
   if (W.fused) {
     evo::BwdFusedLaunch F;
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
@@ -552,7 +537,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.B = (int)d->B; fa.H = d->H; fa.Lq = d->Lq; fa.Lk = d->Lk; fa.D = d->D;
     fa.scale = d->scale; fa.scale_log2 = d->scale * evo::kLog2e;
     // same chunking as the workspace's dbias partials (ws_layout)
-    fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, nk, kNumSMs, &fa.chunk);
+    fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, nk, num_sms(), &fa.chunk);
     fa.bias = (const __nv_bfloat16*)bias;
     fa.b_sh = d->bias_str[1]; fa.b_sq = d->bias_str[2]; fa.b_sk = d->bias_str[3];
     fa.mask = mask; fa.mask_s0 = d->mask_str[0]; fa.mask_s1 = d->mask_str[1];
@@ -563,16 +548,12 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dq_acc = dqacc;
     fa.p_part = (int64_t)d->B * d->H * d->Lq * d->D;
     fa.p_sb = part_str[0]; fa.p_sh = part_str[1]; fa.p_sl = part_str[2];
-    static const int bwd_flags = getenv("EVO_BWD_FLAGS") ? atoi(getenv("EVO_BWD_FLAGS")) : 0;
-    fa.flags = bwd_flags;
     fa.dq_reduce = dq_red ? 1 : 0;
     fa.bmode = bm;
     memset(&F.tm_b, 0, sizeof(F.tm_b));
     if (bm && !make_bias_map(&F.tm_b, d, bias, bm == 1 ? 256 : 128))
       return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for the fused backward's bias map");
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
-    static const bool dbg_timing_b = getenv("EVO_DEBUG_TIMING") != nullptr;
-    fa.dbg = dbg_timing_b ? evo::fwd_debug_ptr() : nullptr;
     if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
     ++nl;
     // fork: the dbias reduce runs on the side stream while dq_convert runs on the caller's
@@ -627,7 +608,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   if (dqacc) {
     evo::ConvertArgs ca{};
     ca.B = (int)d->B; ca.H = d->H; ca.Lq = d->Lq; ca.D = d->D; ca.scale = d->scale; ca.acc = dqacc;
-    ca.nparts = 1; ca.part_stride = 0;  // bwd_main's atomic accumulator: [B,H,Lq,D]
+    ca.nparts = nk;  // bwd_main's per-key-tile parts [nk][B,H,Lq,D], summed in key-tile order
+    ca.part_stride = (int64_t)d->B * d->H * d->Lq * d->D;
     ca.p_sb = (int64_t)d->H * d->Lq * d->D; ca.p_sh = (int64_t)d->Lq * d->D; ca.p_sl = d->D;
     ca.dq = (__nv_bfloat16*)dq; ca.q_sb = d->q_str[0]; ca.q_sh = d->q_str[1]; ca.q_sl = d->q_str[2];
     if ((e = traced(st, "dq_convert", [&] { return evo::launch_dq_convert(ca, st); })) != cudaSuccess) return cuda_fail(e, "dq_convert");

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
   const __nv_bfloat16* o_p = reinterpret_cast<const __nv_bfloat16*>(a.o);
   const __nv_bfloat16* d_p = reinterpret_cast<const __nv_bfloat16*>(a.dout);
   const __nv_bfloat16* g_p = reinterpret_cast<const __nv_bfloat16*>(a.g);
+  const uint64_t zpol = l2_policy_evict_last();
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += 2 * stride) {  // block-uniform trip
     uint4 ov[2], dv[2], gv[2];
     float l[2];
@@ -235,9 +236,9 @@ __global__ void __launch_bounds__(256) bwd_pre_vec_kernel(const BwdPreArgs a) {
       if (!ok[u]) continue;
       if (a.zacc) {
         float4* z = reinterpret_cast<float4*>(a.zacc + zrow[u]);
-        const uint64_t pol = l2_policy_evict_last();  // keep the zeroed lines in L2 for bwd_fused's adds
-        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z), "f"(0.f), "l"(pol) : "memory");
-        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z + 1), "f"(0.f), "l"(pol) : "memory");
+        // evict_last: keep the zeroed lines in L2 for bwd_fused's adds
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z), "f"(0.f), "l"(zpol) : "memory");
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(z + 1), "f"(0.f), "l"(zpol) : "memory");
       }
       if (g_p) {
         *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dA) + arow[u]) =
@@ -265,10 +266,9 @@ cudaError_t launch_bwd_pre(const BwdPreArgs& a, int f32, cudaStream_t st) {
   const int64_t items = (int64_t)a.B * (Lq_pad / 32);
   if (items == 0) return cudaSuccess;
   const int64_t nvec = (int64_t)a.B * a.H * Lq_pad * (a.D / 8);
-  static const bool old_pre = getenv("EVO_BWD_PRE_OLD") != nullptr;  // A/B switch
   // only the vector path zero-fills a dQ accumulator; the caller selects it whenever it asks
-  if (a.zacc && !(!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre)) return cudaErrorInvalidValue;
-  if (!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) && !old_pre) {
+  if (a.zacc && !(!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) )) return cudaErrorInvalidValue;
+  if (!f32 && a.D % 8 == 0 && nvec < ((int64_t)1 << 31) ) {
     BwdPreArgs v = a;
     v.fd_H = make_fastdiv((uint32_t)a.H);
     v.fd_Lq = make_fastdiv((uint32_t)a.Lq);
@@ -529,11 +529,14 @@ __global__ void __launch_bounds__(256, 1) bwd_main_kernel(const __grid_constant_
           *reinterpret_cast<uint4*>(a.dq + (int64_t)b * a.q_sb + (int64_t)h * a.q_sh +
                                     (int64_t)q * a.q_sl + d0) = st;
         } else {
-          float4* dst = reinterpret_cast<float4*>(a.dq_acc + ((int64_t)bh * a.Lq + q) * a.D + d0);
-          atomicAdd(dst, make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]),
-                                     __uint_as_float(r[2]), __uint_as_float(r[3])));
-          atomicAdd(dst + 1, make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]),
-                                         __uint_as_float(r[6]), __uint_as_float(r[7])));
+          // this key tile's own fp32 part (plain stores): dq_convert sums the nk parts in
+          // key-tile order, so dq does not depend on the CTAs' completion order
+          float4* dst = reinterpret_cast<float4*>(
+              a.dq_acc + ((int64_t)j * a.B * a.H + bh) * (int64_t)a.Lq * a.D + (int64_t)q * a.D + d0);
+          dst[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
+                               __uint_as_float(r[3]));
+          dst[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]),
+                               __uint_as_float(r[7]));
         }
       }
     }
@@ -574,7 +577,7 @@ template <int DP, int BIAS>
 static cudaError_t launch_bwd_main_t(const BwdMainLaunch& L, cudaStream_t st) {
   auto kern = bwd_main_kernel<DP, BIAS>;
   const size_t smem = bwd_main_smem_bytes(DP);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.B * L.args.H * nk;
@@ -767,7 +770,7 @@ template <int DP, int BIAS>
 static cudaError_t launch_bwd_bias_t(const BwdBiasLaunch& L, cudaStream_t st) {
   auto kern = bwd_bias_kernel<DP, BIAS>;
   const size_t smem = bwd_bias_smem_bytes(DP);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nq = (L.args.Lq + 127) / 128, nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nq * nk * L.args.nchunks;
@@ -905,6 +908,7 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
   const uint32_t n8 = rows * (uint32_t)nd;
   const bool hfast = a.q_sh < a.q_sl;
   (void)ND;
+  const uint64_t pol = l2_policy_evict_first();
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n8; idx += gridDim.x * blockDim.x) {
     uint32_t r = fdiv(idx, a.fd_nd), r2;
     const uint32_t d0 = (idx - r * (uint32_t)nd) * 8;
@@ -917,12 +921,14 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const ConvertArgs a) {
       r2 = fdiv(r, a.fd_H); h = r - r2 * (uint32_t)a.H; r = r2;
     }
     const int64_t b = r;
+    // last read of the fp32 accumulator / parts: evict_first, so these lines (left at
+    // evict_last by bwd_pre's zero-fill and the reduce-adds) do not crowd the next kernels out
     const float* src = a.acc + b * a.p_sb + (int64_t)h * a.p_sh + (int64_t)q * a.p_sl + d0;
-    float4 x = __ldg(reinterpret_cast<const float4*>(src));
-    float4 y = __ldg(reinterpret_cast<const float4*>(src) + 1);
-    for (int p = 1; p < a.nparts; ++p) {
-      const float4 x2 = __ldg(reinterpret_cast<const float4*>(src + p * a.part_stride));
-      const float4 y2 = __ldg(reinterpret_cast<const float4*>(src + p * a.part_stride) + 1);
+    float4 x = ldg_f4_hint(src, pol);
+    float4 y = ldg_f4_hint(src + 4, pol);
+    for (int p = 1; p < a.nparts; ++p) {  // parts summed in key-tile order (deterministic)
+      const float4 x2 = ldg_f4_hint(src + p * a.part_stride, pol);
+      const float4 y2 = ldg_f4_hint(src + p * a.part_stride + 4, pol);
       x.x += x2.x; x.y += x2.y; x.z += x2.z; x.w += x2.w;
       y.x += y2.x; y.y += y2.y; y.z += y2.z; y.w += y2.w;
     }

@@ -97,8 +97,6 @@ __global__ void __launch_bounds__(384, 1)
   const int nb = min(a.B - b0, a.chunk);
   if (nb <= 0) return;
   const int J = nb * nq * 4;  // 32-query sub-tiles
-  unsigned long long* dbg = (a.dbg && blockIdx.x < 4) ? a.dbg + blockIdx.x * 4096 : nullptr;
-#define DBG(i) do { if (dbg) dbg[i] = clock64(); } while (0)
 
   if (w == 0) tmem_alloc<512>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -172,7 +170,6 @@ __global__ void __launch_bounds__(384, 1)
         const int T = sbi * nq + stt, st = T & 1, kvs = sbi & 1;
         if (sss == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
         if (sss == 0 && stt == 0) mbar_wait(bar_kv + 8 * kvs, (sbi >> 1) & 1);
-        if (j < 256) DBG(2048 + j * 4 + 0);
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + sss * 32 * C::kRowBytes;
@@ -208,7 +205,6 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(bar_ps + 8 * g, (i >> 1) & 1);
         // the first sub-tile of a new batch row overwrites dK/dV: group 0 must have pulled them
         if (dtt == 0 && dss == 0 && dbi > 0) mbar_wait(bar_dkvfree, (dbi - 1) & 1);
-        if (i < 256) DBG(2048 + i * 4 + 1);
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
         const uint32_t ab = qb + C::kTile;
@@ -526,7 +522,6 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   }
-#undef DBG
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
@@ -536,7 +531,7 @@ template <int DP, bool BIAS>
 static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) {
   auto kern = bwd_fused_kernel<DP, BIAS>;
   const size_t smem = FusedCfg<DP, BIAS>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;

@@ -6,6 +6,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #define EVO_DEV __device__ __forceinline__
 
 namespace evo {
@@ -115,6 +119,19 @@ EVO_DEV uint64_t l2_policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+EVO_DEV uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// read-only 16-byte load with an L2 cache policy (e.g. evict_first for a last read)
+EVO_DEV float4 ldg_f4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
 }
 EVO_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the issuing thread's bulk groups have finished READING shared memory
@@ -391,6 +408,36 @@ EVO_DEV void umma_commit(uint32_t bar) {
 EVO_DEV uint32_t swz_offset(uint32_t row, uint32_t chunk, uint32_t row_bytes) {
   uint32_t sh = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
   return row * row_bytes + ((chunk ^ ((row & 7u) >> sh)) << 4);
+}
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device) instead of on every
+// launch (the attribute is per function and device; a larger request raises it again).  Keyed
+// on the kernel's address: different instantiations share one function-pointer type.
+inline cudaError_t set_smem_once_impl(const void* kern, size_t smem) {
+  struct Entry {
+    const void* kern;
+    int dev;
+    size_t smem;  // the largest limit set so far
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  Entry* hit = nullptr;
+  for (auto& x : done)
+    if (x.kern == kern && x.dev == dev) hit = &x;
+  if (hit && hit->smem >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (hit) hit->smem = smem;
+  else done.push_back({kern, dev, smem});
+  return e;
+}
+template <class K>
+inline cudaError_t set_smem_once(K kern, size_t smem) {
+  return set_smem_once_impl(reinterpret_cast<const void*>(kern), smem);
 }
 
 }  // namespace evo

@@ -1,7 +1,7 @@
 // evo_fwd_occ.cu — occupancy-based bf16 forward (sm_100a): one (b, h, 128-query tile) unit per
 // 128-thread CTA, four CTAs per SM.
 //
-// Same operation as evo_fwd.cu (pair bias added to the logits before the softmax,
+// Same operation as the oracle's forward (pair bias added to the logits before the softmax,
 // all of MHA fused, FlashAttention-style online softmax).  At head dim 32 the exp (MUFU) pipe
 // binds, so the design goal is simply "always have a warp with exps ready": each SM runs four
 // independent units whose softmax warps the hardware scheduler interleaves, instead of a
@@ -9,8 +9,8 @@
 //
 // Per CTA (thread = query row = TMEM lane; thread 0 also issues TMA and tcgen05.mma):
 //   TMEM (128 cols for D <= 32):  S|P [0,64)  O [64, 64+DP)  Q [96, 96+DP/2)  (G [.., +DP/2)
-//   only with EVO_FWD_FLAGS bit 1: the gate row is otherwise prefetched to L2 and read in the
-//   epilogue)
+//   only with two key chunks or fewer: the gate row is otherwise prefetched to L2 and read in
+//   the epilogue)
 //   Q row -> TMEM once (tcgen05.st), then per 64-key chunk c (K/V/bias double-buffered by TMA):
 //     S  = Q·K_cᵀ            tcgen05.mma, A = Q from TMEM (TS form), N = 64
 //     x  = S·scale + bias    f32x2 FMA; hard mask; chunk max (3-input max)
@@ -125,13 +125,13 @@ __global__ void __launch_bounds__(128, 4)
   // here hides its latency behind the key loop) instead of with the Q row into TMEM: L = 256
   // forward 54.2 / 55.3 / 63.5 -> 51.2 / 51.3 / 57.3 us (row / start / end).  Two chunks are
   // too short to hide it (MSA column, L = 128: 36.9 early vs 38.9 late), so the gate rides with
-  // Q there.  EVO_FWD_FLAGS bit 1 forces the prologue load.
-  const bool late_g = nc > 2 && (a.flags & 2) == 0;
+  // Q there.
+  const bool late_g = nc > 2;
   {
     uint32_t qrow[DP / 2], gpk[DP / 2];
     const __nv_bfloat16* qp = qptr + (int64_t)b * q_sb + (int64_t)h * q_sh + (int64_t)q * q_sl;
     const __nv_bfloat16* gp = a.g + (int64_t)b * a.g_sb + (int64_t)h * a.g_sh + (int64_t)q * a.g_sl;
-    if (late_g && a.g && qv && !(a.flags & 4)) prefetch_l2(gp);  // loaded in the epilogue
+    if (late_g && a.g && qv) prefetch_l2(gp);  // loaded in the epilogue
 #pragma unroll
     for (int d0 = 0; d0 < DP; d0 += 8) {
       uint4 v = make_uint4(0, 0, 0, 0), gv = make_uint4(0, 0, 0, 0);
@@ -381,7 +381,7 @@ template <int DP, int BIAS>
 static cudaError_t launch_fwd_occ_t(const FwdOccLaunch& L, cudaStream_t st) {
   auto kern = fwd_occ_kernel<DP, BIAS>;
   const size_t smem = OccCfg<DP, BIAS>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const long long grid = (long long)L.args.B * L.args.H * ((L.args.Lq + 127) / 128);
   if (grid == 0) return cudaSuccess;

@@ -398,11 +398,11 @@ template <int D>
 static cudaError_t ga_launch(const GaArgs& a, bool bwd, cudaStream_t st) {
   const size_t smem = ga_smem<D>(a, bwd);
   if (bwd) {
-    cudaError_t e = cudaFuncSetAttribute(global_attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem_once(global_attn_bwd_kernel<D>, smem);
     if (e != cudaSuccess) return e;
     global_attn_bwd_kernel<D><<<(unsigned)a.B, kGaThreads, smem, st>>>(a);
   } else {
-    cudaError_t e = cudaFuncSetAttribute(global_attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem_once(global_attn_fwd_kernel<D>, smem);
     if (e != cudaSuccess) return e;
     global_attn_fwd_kernel<D><<<(unsigned)a.B, kGaThreads, smem, st>>>(a);
   }

@@ -39,21 +39,8 @@ struct FwdArgs {
   __nv_bfloat16* o;
   int64_t o_sb, o_sh, o_sl;
   float* lse;
-  unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
-  int flags;                // experiment switches (EVO_FWD_FLAGS), 0 in production
 };
-struct FwdLaunch {
-  CUtensorMap tm_q, tm_k, tm_v, tm_b;
-  FwdArgs args;
-};
-inline size_t fwd_smem_bytes(int DP) {
-  return 5 * 128 * (size_t)DP * 2 + 65536 + kMaxMaskWords * 4 + 2 * 256 * 4 + 8 * 8 + 16;
-}
-cudaError_t launch_fwd_bf16(const FwdLaunch& L, int DP, int bias_mode, cudaStream_t st);
-// persistent warp-specialised forward (evo_fwd_ws.cu)
-cudaError_t launch_fwd_ws_bf16(const FwdLaunch& L, int DP, int bias_mode, cudaStream_t st);
-unsigned long long* fwd_debug_ptr();
-// occupancy-based forward (evo_fwd_occ.cu): K/V maps with 64-row boxes, Q read by threads
+// forward (evo_fwd_occ.cu): K/V maps with 64-row boxes, Q read by threads
 struct FwdOccLaunch {
   CUtensorMap tm_k, tm_v, tm_b;
   FwdArgs args;
@@ -61,12 +48,6 @@ struct FwdOccLaunch {
   int64_t q_sb, q_sh, q_sl;
 };
 cudaError_t launch_fwd_occ_bf16(const FwdOccLaunch& L, int DP, int bias_mode, cudaStream_t st);
-// ping-pong persistent forward (evo_fwd_pp.cu): Q and G by TMA (128-row boxes), K/V 64-row boxes
-struct FwdPpLaunch {
-  CUtensorMap tm_q, tm_g, tm_k, tm_v, tm_b;
-  FwdArgs args;
-};
-cudaError_t launch_fwd_pp_bf16(const FwdPpLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
 // ------------------------------------------------------------------ backward (bf16)
 struct BwdPreArgs {  // D_q, lse2, dA, dg  (all rows of [B,H,Lq])
@@ -103,7 +84,8 @@ struct BwdMainArgs {  // dK, dV (and dQ partials) — CTA per (b, h, key tile)
   int64_t v_sb, v_sh, v_sl;
   __nv_bfloat16* dq;  // direct store when there is a single key tile
   int64_t q_sb, q_sh, q_sl;
-  float* dq_acc;      // [B,H,Lq,D] fp32 accumulator otherwise
+  float* dq_acc;      // otherwise nk fp32 parts [nk][B,H,Lq,D] (plain stores; dq_convert sums
+                      // them in key-tile order, so dq is bitwise deterministic)
 };
 struct BwdMainLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
@@ -154,12 +136,13 @@ struct BwdFusedArgs {
   int64_t v_sb, v_sh, v_sl;
   __nv_bfloat16* dq;  // direct store when there is a single key tile
   int64_t q_sb, q_sh, q_sl;
-  float* dq_acc;      // otherwise nk fp32 parts: key tile kt's dQ part (plain stores) at
+  float* dq_acc;      // otherwise fp32: dq_reduce ? ONE accumulator every key tile reduce-adds
+                      // into : nk parts, key tile kt's part (plain stores) at
   int64_t p_part, p_sb, p_sh, p_sl;  // dq_acc + kt*p_part + b*p_sb + h*p_sh + q*p_sl
   float* partial;     // [nchunks][H][Lq_pad][Lk_pad] fp32 dbias partials
-  unsigned long long* dbg;  // optional phase timestamps (EVO_DEBUG_TIMING), else NULL
-  int flags;  // experiment switches (EVO_BWD_FLAGS), 0 in production
-  int dq_reduce;  // 1: every key tile reduce-adds its dQ into ONE fp32 accumulator (zeroed by bwd_pre)
+  int dq_reduce;  // 1 (only when nk == 2, so 0 + a + b is order-independent and dq stays bitwise
+                  // deterministic): both key tiles reduce-add into ONE fp32 accumulator (zeroed
+                  // by bwd_pre); 0: one part per key tile, summed in key-tile order by dq_convert
   int bmode;  // bias: 1 k-contiguous (tm_b box [256 q][64 k]), 2 q-contiguous (box [128 k][64 q])
 };
 struct BwdFusedLaunch {

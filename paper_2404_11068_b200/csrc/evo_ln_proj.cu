@@ -482,8 +482,7 @@ static evo_status_t ln_proj_launch(const evo_ln_proj_desc_t* d, const void* x, c
 #define EVO_LP_CASE(CC)                                                                      \
   case CC:                                                                                   \
     cfg.dynamicSmemBytes = lp_smem<CC>();                                                    \
-    e = cudaFuncSetAttribute(ln_proj_fwd_kernel<CC>,                                         \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem<CC>()); \
+    e = evo::set_smem_once(ln_proj_fwd_kernel<CC>, lp_smem<CC>());                         \
     if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, ln_proj_fwd_kernel<CC>, tx, tw, to, a); \
     break;
     EVO_LP_CASE(64)

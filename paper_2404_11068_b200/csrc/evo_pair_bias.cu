@@ -538,8 +538,7 @@ inline int64_t pb_warps(const PbArgs& a) { return (a.Li * a.Lj + kRowsPerWarp - 
 template <int C>
 static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
   const int64_t rows = a.Li * a.Lj;
-  static const bool warp_rows = getenv("EVO_PB_FWD_WARP") != nullptr;  // A/B: warp-per-row kernel
-  if (!warp_rows && rows < ((int64_t)1 << 31)) {
+  if (rows < ((int64_t)1 << 31)) {  // else the warp-per-row kernel (64-bit row indices)
     const unsigned grid = (unsigned)((rows + 127) / 128);  // 128 rows (two threads each) per block
     const FastDiv fd = make_fastdiv((uint32_t)a.Lj);
     if (a.H == 4) pair_bias_fwd_row_kernel<C, 4><<<grid, 256, 0, st>>>(a, fd);
@@ -557,14 +556,13 @@ static cudaError_t launch_fwd_c(const PbArgs& a, cudaStream_t st) {
 
 template <int C, int H>
 static cudaError_t launch_bwd_ch(const PbArgs& a, cudaStream_t st) {
-  static const bool warp_rows = getenv("EVO_PB_BWD_WARP") != nullptr;  // A/B: warp-per-row kernel
-  if constexpr (C <= 128) {
-    if (!warp_rows && a.Li * a.Lj < ((int64_t)1 << 31)) {
+  if constexpr (C <= 128) {  // else (c_z = 256, or 2^31 rows) the warp-per-row kernel
+    if (a.Li * a.Lj < ((int64_t)1 << 31)) {
       // 128 rows per block: the same block count (and partial layout) as the warp kernel
       const unsigned grid = (unsigned)((a.Li * a.Lj + 127) / 128);
       auto k = pair_bias_bwd_row_kernel<C, H>;
       constexpr size_t smem = (2 * (C / 2 * H + 4) + 128 * (C + 1) + 128 * H + C * (H + 2)) * 4;
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = set_smem_once(k, smem);
       if (e != cudaSuccess) return e;
       k<<<grid, 256, smem, st>>>(a, make_fastdiv((uint32_t)a.Lj));
       return cudaGetLastError();
@@ -573,7 +571,7 @@ static cudaError_t launch_bwd_ch(const PbArgs& a, cudaStream_t st) {
   const unsigned grid = (unsigned)((pb_warps(a) + 7) / 8);
   auto k = pair_bias_bwd_kernel<C, H>;
   constexpr size_t smem = 8 * (C * H + 2 * C) * 4;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(k, smem);
   if (e != cudaSuccess) return e;
   k<<<grid, 256, smem, st>>>(a);
   return cudaGetLastError();

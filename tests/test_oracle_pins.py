@@ -153,6 +153,7 @@ def test_p3_single_key():
 def test_p4_masked_keys_inert():
     c = _case(B=3, H=2, L=9, D=4, seed=5, mask="prefix")
     c["mask"][1, 3] = 0  # an interior hole too
+    c["mask"][:, 7] = 0  # a key masked in EVERY batch row: its (shared) bias column is inert too
     f = oracle.attn_fwd(c["q"], c["k"], c["v"], bias=c["bias"], mask=c["mask"], g=c["g"],
                         scale=c["scale"])
     gr = oracle.attn_bwd(c["q"], c["k"], c["v"], c["dout"], bias=c["bias"], mask=c["mask"],
@@ -164,6 +165,11 @@ def test_p4_masked_keys_inert():
         for kk in np.nonzero(dropped[b])[0]:
             k2[b, :, kk] = rng.standard_normal(k2[b, :, kk].shape) * 100
             v2[b, :, kk] = rng.standard_normal(v2[b, :, kk].shape) * 100
+    # the shared bias is read by every batch row, so only the columns of keys masked in all
+    # rows can be re-randomised (reading R5: masked keys never influence any output)
+    all_dropped = np.nonzero(dropped.all(axis=0))[0]
+    assert all_dropped.size > 0
+    b2[:, :, all_dropped] = rng.standard_normal(b2[:, :, all_dropped].shape) * 100
     f2 = oracle.attn_fwd(c["q"], k2, v2, bias=b2, mask=c["mask"], g=c["g"], scale=c["scale"])
     gr2 = oracle.attn_bwd(c["q"], k2, v2, c["dout"], bias=b2, mask=c["mask"], g=c["g"],
                           scale=c["scale"])
