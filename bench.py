@@ -399,6 +399,8 @@ def run_gpu(args):
     e2e = run_e2e(torch, evoattn, mods, args, dev, stream, flops)
 
     cpu = cpu_baseline(args.cpu_seconds) if not args.no_cpu else None
+    configs = None if args.no_configs else run_configs(
+        torch, evoattn, dev, flush, max(3, min(args.steps, 10)), clk.get("sm_mhz"))
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -419,8 +421,156 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "cpu_baseline": cpu,
+        "configs": configs,
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- other configs
+# BASELINE.json configs[0], [3], [4] and the §8(f) side paths, timed in the same run so their
+# numbers come from the driver's box (not only from builder tools): device time per call with
+# CUDA events on the launching stream, L2 flushed before every call, median over `reps`.
+# (name, B, H, L, D, bias, storage "bl" [B,L,H,D] | "lb" [L,B,H,D], bias q-contiguous)
+CONFIGS = [
+    ("cfg1_tri_start_nres32", 32, 2, 32, 16, True, "bl", False),
+    ("cfg4_extra_msa_col_nextra1024", 256, 8, 1024, 8, False, "lb", False),
+    ("f3_extra_msa_row_nextra1024", 1024, 8, 256, 8, True, "bl", False),
+    ("cfg5_row_nres384_nseq512", 512, 8, 384, 32, True, "bl", False),
+    ("cfg5_col_nres384_nseq512", 384, 8, 512, 32, False, "lb", False),
+    ("cfg5_start_nres384", 384, 4, 384, 32, True, "bl", False),
+    ("cfg5_end_nres384", 384, 4, 384, 32, True, "lb", True),
+]
+
+
+def _cfg_inputs(torch, dev, B, H, L, D, bias, st, bt, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    shape, perm = ((B, L, H, D), (0, 2, 1, 3)) if st == "bl" else ((L, B, H, D), (1, 2, 0, 3))
+    t = {n: torch.randn(shape, generator=g).to(dev, torch.bfloat16).permute(*perm)
+         for n in ("q", "k", "v", "g", "dout")}
+    t["bias"] = None
+    if bias:
+        b = torch.randn((H, L, L), generator=g).to(dev, torch.bfloat16)
+        t["bias"] = b.transpose(1, 2) if bt else b
+    m = torch.ones((B, L), dtype=torch.uint8)
+    t["mask"] = m.t().contiguous().to(dev).t() if st == "lb" else m.to(dev)
+    return t
+
+
+def _timed(torch, fn, flush, reps):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+
+def run_configs(torch, evoattn, dev, flush, reps, clk_mhz):
+    """One entry per config: fwd / bwd / fwd+bwd ms, algorithmic TFLOP/s and the three roofline
+    fractions of the call (tensor = 12·B·H·L²·D flops vs the measured bf16 peak, HBM = the
+    algorithmic bytes of DESIGN.md §5 vs the measured copy bandwidth, MUFU = 2·B·H·L² exps vs
+    148 x 16 ex2/clk at the sampled clock), with the binding one named."""
+    pk = measured_peaks()
+    mufu = 148 * 16 * (clk_mhz or pk["sm_max_mhz"]) * 1e6
+    out = {}
+    for i, (name, B, H, L, D, bias, st, bt) in enumerate(CONFIGS):
+        t = _cfg_inputs(torch, dev, B, H, L, D, bias, st, bt, seed=200 + i)
+        ws = torch.empty(max(1, evoattn.workspace_bytes(t["q"], t["k"], t["v"], t["bias"],
+                                                        t["mask"], t["g"])),
+                         dtype=torch.uint8, device=dev)
+        f = lambda: evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
+        o, lse = f()
+        bw = lambda: evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"],
+                                 t["mask"], t["g"], workspace=ws)
+        for _ in range(3):
+            f()
+            bw()
+        torch.cuda.synchronize()
+        tf, tb = _timed(torch, f, flush, reps), _timed(torch, bw, flush, reps)
+        tfb = _timed(torch, lambda: (f(), bw()), flush, reps)
+        X, P = B * H * L * D, B * H * L * L
+        bb = 2 * H * L * L if bias else 0
+        byt = 30.0 * X + 4.0 * bb + 2 * B * L + 8 * B * H * L  # fwd + bwd bytes (DESIGN §5)
+        fl = alg_flops(B, H, L, D)
+        fr = {"tensor": fl / (tfb * 1e-3) / 1e12 / pk["bf16_tflops"],
+              "hbm": byt / (tfb * 1e-3) / 1e9 / pk["hbm_gbs"],
+              "mufu": 2.0 * P / (tfb * 1e-3) / mufu}
+        out[name] = {"B": B, "H": H, "L": L, "D": D, "bias": bias, "fwd_ms": tf, "bwd_ms": tb,
+                     "fwd_bwd_ms": tfb, "tflops_alg": fl / (tfb * 1e-3) / 1e12,
+                     "fracs": fr, "binding": max(fr, key=fr.get)}
+        del t, ws, o, lse
+    # cfg 5 per block: the four modules at N_res = 384, N_seq = 512
+    c5 = [k for k in out if k.startswith("cfg5_")]
+    out["cfg5_block_nres384_nseq512"] = {
+        "ms_per_block": sum(out[k]["fwd_bwd_ms"] for k in c5),
+        "ms_per_48_block_stack": 48 * sum(out[k]["fwd_bwd_ms"] for k in c5),
+        "tflops_alg": sum(alg_flops(out[k]["B"], out[k]["H"], out[k]["L"], out[k]["D"])
+                          for k in c5) / (sum(out[k]["fwd_bwd_ms"] for k in c5) * 1e-3) / 1e12,
+        "note": "sum of the four module calls timed one by one (L2 flushed before each)"}
+    out.update(run_side_paths(torch, evoattn, dev, flush, reps, pk))
+    return out
+
+
+def run_side_paths(torch, evoattn, dev, flush, reps, pk):
+    """§8(f) side paths at the N_res = 256 block shapes: f1 pair bias (LN(z)·W, fwd + bwd), f2
+    LN + stacked q|k|v|g projection, f3 extra-MSA global column attention (fwd + bwd)."""
+    out = {}
+    L, C = 256, 128
+    for H in (4, 8):
+        z = torch.randn((L, L, C), device=dev).to(torch.bfloat16)
+        gamma, beta = torch.ones(C, device=dev), torch.zeros(C, device=dev)
+        W = torch.randn((C, H), device=dev) / C ** 0.5
+        dbias = torch.randn((H, L, L), device=dev)
+        bias, mean, rstd = evoattn.pair_bias_fwd(z, gamma, beta, W)
+        ws = torch.empty(1 << 24, dtype=torch.uint8, device=dev)
+        f = lambda: evoattn.pair_bias_fwd(z, gamma, beta, W)
+        b = lambda: evoattn.pair_bias_bwd(z, gamma, beta, W, mean, rstd, dbias, workspace=ws)
+        for _ in range(3):
+            f()
+            b()
+        tf, tb = _timed(torch, f, flush, reps), _timed(torch, b, flush, reps)
+        byf = L * L * C * 2 + H * L * L * 2 + 8 * L * L
+        byb = 2 * L * L * C * 2 + H * L * L * 4 + 8 * L * L
+        out[f"f1_pair_bias_nres256_cz128_h{H}"] = {
+            "fwd_ms": tf, "bwd_ms": tb, "fwd_hbm_frac": byf / (tf * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "bwd_hbm_frac": byb / (tb * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    for name, rows, C, N in [("msa", 128 * 256, 256, 1024), ("triangle", 256 * 256, 128, 512),
+                             ("extra_msa", 1024 * 256, 64, 256)]:
+        x = torch.randn((rows, C), device=dev).to(torch.bfloat16)
+        g, bt = torch.ones(C, device=dev), torch.zeros(C, device=dev)
+        W = (torch.randn((N, C), device=dev) / C ** 0.5).to(torch.bfloat16)
+        bb = torch.zeros(N, device=dev)
+        o = torch.empty((rows, N), dtype=torch.bfloat16, device=dev)
+        f = lambda: evoattn.ln_proj_fwd(x, g, bt, W, bb, out=o)
+        for _ in range(3):
+            f()
+        tf = _timed(torch, f, flush, reps)
+        byt = rows * C * 2 + rows * N * 2 + N * C * 2 + rows * 8
+        out[f"f2_ln_qkvg_proj_{name}_{rows}x{C}to{N}"] = {
+            "fwd_ms": tf, "tflops": 2.0 * rows * C * N / (tf * 1e-3) / 1e12,
+            "hbm_frac": byt / (tf * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    B, S, H, D = 256, 1024, 8, 8
+    gq = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+    gg = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+    gk = torch.randn((S, B, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+    gv = torch.randn((S, B, D), device=dev).to(torch.bfloat16).transpose(0, 1)
+    gm = torch.ones((S, B), dtype=torch.uint8, device=dev).t()
+    o, lse, qbar = evoattn.global_attn_fwd(gq, gk, gv, gg, gm)
+    f = lambda: evoattn.global_attn_fwd(gq, gk, gv, gg, gm)
+    b = lambda: evoattn.global_attn_bwd(gq, gk, gv, gg, lse, qbar, o, gm)
+    for _ in range(3):
+        f()
+        b()
+    tf, tb = _timed(torch, f, flush, reps), _timed(torch, b, flush, reps)
+    byf = (2 * B * S * H * D + 2 * B * S * D) * 2 + B * S * H * D * 2
+    byb = (3 * B * S * H * D + 2 * B * S * D) * 2 + (2 * B * S * H * D + 2 * B * S * D) * 2
+    out["f3_global_col_attn_nres256_nextra1024"] = {
+        "fwd_ms": tf, "bwd_ms": tb, "fwd_hbm_frac": byf / (tf * 1e-3) / 1e9 / pk["hbm_gbs"],
+        "bwd_hbm_frac": byb / (tb * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    return out
 
 
 def load_traffic(kernel):
@@ -509,6 +659,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a graph")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs / side paths (the `configs` key)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=2,
                     help="--impl reference: batch rows of each module per step")

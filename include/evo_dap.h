@@ -97,6 +97,15 @@ evo_status_t evo_dap_pack(const void* src, void* dst, int32_t n, int64_t A_loc, 
 evo_status_t evo_dap_barrier(evo_dap_t* dap, float* scratch /* 1 float, device */,
                              void* stream);
 
+/* Wait for the work enqueued on `stream` (a cudaStream_t) while polling the communicator for an
+ * asynchronous NCCL error (ncclCommGetAsyncError): returns EVO_OK once the stream is idle;
+ * on an asynchronous error, or when `timeout_s` > 0 seconds pass first (a peer rank died or
+ * hangs), aborts the communicator (ncclCommAbort; every later collective call on `dap` fails
+ * with EVO_E_INVALID) and returns EVO_E_CUDA with the rank and reason in
+ * evo_dap_last_error_detail().  Host-blocking; use it instead of a bare stream synchronise
+ * around DAP steps (SURVEY.md §5 failure detection). */
+evo_status_t evo_dap_wait(evo_dap_t* dap, void* stream, double timeout_s);
+
 const char* evo_dap_last_error_detail(void);
 
 #ifdef __cplusplus

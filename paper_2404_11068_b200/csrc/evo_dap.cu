@@ -13,11 +13,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "evo_dap.h"
 
@@ -52,33 +54,41 @@ evo_status_t cuda_check(cudaError_t e, const char* what) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// dst[y][x][:] = src[x][y][:] over rows of W16 16-byte vectors.
+// dst[y][x][:] = src[x][y][:] over rows of W16 16-byte vectors.  `tpr` threads (a power of two
+// dividing the block) share one output row, so the row's (x, y) decomposition is one integer
+// division per thread per row — amortised over W16 / tpr vectors — instead of a 64-bit
+// division/modulo per 16-byte element.
 __global__ void __launch_bounds__(256) swap01_kernel(const uint4* __restrict__ src,
                                                      uint4* __restrict__ dst, int64_t X,
-                                                     int64_t Y, int64_t W16) {
-  const int64_t total = X * Y * W16;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t w = o % W16;
-    const int64_t r = o / W16;  // output row = y * X + x
-    const int64_t x = r % X, y = r / X;
-    dst[o] = __ldg(&src[(x * Y + y) * W16 + w]);
+                                                     int64_t Y, int64_t W16, int tpr) {
+  const int64_t rows = X * Y;
+  const int rpb = blockDim.x / tpr;  // rows per block per iteration
+  const int sub = threadIdx.x % tpr;
+  for (int64_t r = (int64_t)blockIdx.x * rpb + threadIdx.x / tpr; r < rows;
+       r += (int64_t)gridDim.x * rpb) {
+    const int64_t y = r / X, x = r - y * X;  // output row r = y * X + x
+    const uint4* s = src + (x * Y + y) * W16;
+    uint4* d = dst + r * W16;
+    for (int64_t w = sub; w < W16; w += tpr) d[w] = __ldg(&s[w]);
   }
 }
 
 evo_status_t launch_swap01(const void* src, void* dst, int64_t X, int64_t Y, int64_t W_bytes,
                            cudaStream_t st) {
   const int64_t W16 = W_bytes / 16;
-  const int64_t total = X * Y * W16;
-  if (total == 0) return EVO_OK;
+  const int64_t rows = X * Y;
+  if (rows * W16 == 0) return EVO_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t blocks = (total + 255) / 256;
+  int tpr = 1;
+  while (tpr < 256 && tpr < W16) tpr <<= 1;
+  const int64_t rpb = 256 / tpr;
+  int64_t blocks = (rows + rpb - 1) / rpb;
   const int64_t cap = (int64_t)sms * 8;  // 8 resident 256-thread CTAs per SM
   if (blocks > cap) blocks = cap;
   swap01_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint4*>(src),
-                                                   static_cast<uint4*>(dst), X, Y, W16);
+                                                   static_cast<uint4*>(dst), X, Y, W16, tpr);
   return cuda_check(cudaGetLastError(), "swap01 launch");
 }
 
@@ -118,7 +128,7 @@ evo_status_t evo_dap_init(int32_t nranks, int32_t rank, const void* uid, int32_t
 
 evo_status_t evo_dap_destroy(evo_dap_t* dap) {
   if (!dap) return EVO_OK;
-  evo_status_t s = nccl_check(ncclCommDestroy(dap->comm), "ncclCommDestroy");
+  evo_status_t s = dap->comm ? nccl_check(ncclCommDestroy(dap->comm), "ncclCommDestroy") : EVO_OK;
   delete dap;
   return s;
 }
@@ -151,7 +161,7 @@ evo_status_t evo_dap_pack(const void* src, void* dst, int32_t n, int64_t A_loc, 
 evo_status_t evo_dap_alltoall_transpose(evo_dap_t* dap, const void* src, void* dst, void* staging,
                                         size_t staging_bytes, int64_t A, int64_t Bd,
                                         int64_t C_bytes, int32_t dir, void* stream) {
-  if (!dap) return fail(EVO_E_INVALID, "dap is NULL");
+  if (!dap || !dap->comm) return fail(EVO_E_INVALID, "dap is NULL or its communicator was aborted");
   const int n = dap->nranks;
   if (A < 0 || Bd < 0 || C_bytes < 0) return fail(EVO_E_SHAPE, "negative extent");
   if (A % n || Bd % n)
@@ -188,7 +198,7 @@ evo_status_t evo_dap_alltoall_transpose(evo_dap_t* dap, const void* src, void* d
 
 evo_status_t evo_dap_allgather(evo_dap_t* dap, const void* src, void* dst, size_t bytes_per_rank,
                                void* stream) {
-  if (!dap) return fail(EVO_E_INVALID, "dap is NULL");
+  if (!dap || !dap->comm) return fail(EVO_E_INVALID, "dap is NULL or its communicator was aborted");
   if (bytes_per_rank == 0) return EVO_OK;
   if (!src || !dst) return fail(EVO_E_INVALID, "NULL buffer");
   if (bytes_per_rank % 16 || !aligned16(src) || !aligned16(dst))
@@ -200,7 +210,7 @@ evo_status_t evo_dap_allgather(evo_dap_t* dap, const void* src, void* dst, size_
 
 evo_status_t evo_dap_reduce_scatter_f32(evo_dap_t* dap, const float* src, float* dst,
                                         size_t count_per_rank, void* stream) {
-  if (!dap) return fail(EVO_E_INVALID, "dap is NULL");
+  if (!dap || !dap->comm) return fail(EVO_E_INVALID, "dap is NULL or its communicator was aborted");
   if (count_per_rank == 0) return EVO_OK;
   if (!src || !dst) return fail(EVO_E_INVALID, "NULL buffer");
   if (!aligned16(src) || !aligned16(dst)) return fail(EVO_E_ALIGN, "buffer not 16-byte aligned");
@@ -209,8 +219,36 @@ evo_status_t evo_dap_reduce_scatter_f32(evo_dap_t* dap, const float* src, float*
                     "ncclReduceScatter");
 }
 
+evo_status_t evo_dap_wait(evo_dap_t* dap, void* stream, double timeout_s) {
+  if (!dap || !dap->comm) return fail(EVO_E_INVALID, "dap is NULL or its communicator was aborted");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(dap->comm, &ar);
+    if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+      ncclCommAbort(dap->comm);
+      dap->comm = nullptr;
+      return fail(EVO_E_CUDA, "NCCL asynchronous error on rank %d: %s (communicator aborted)",
+                  dap->rank, ncclGetErrorString(r != ncclSuccess ? r : ar));
+    }
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return EVO_OK;
+    if (q != cudaErrorNotReady) return cuda_check(q, "cudaStreamQuery");
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) {
+      ncclCommAbort(dap->comm);
+      dap->comm = nullptr;
+      return fail(EVO_E_CUDA, "rank %d: stream not done after %.1f s (a peer is missing or "
+                  "hung; communicator aborted)", dap->rank, el);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 evo_status_t evo_dap_barrier(evo_dap_t* dap, float* scratch, void* stream) {
-  if (!dap) return fail(EVO_E_INVALID, "dap is NULL");
+  if (!dap || !dap->comm) return fail(EVO_E_INVALID, "dap is NULL or its communicator was aborted");
   if (!scratch) return fail(EVO_E_INVALID, "scratch is NULL");
   return nccl_check(ncclAllReduce(scratch, scratch, 1, ncclFloat32, ncclSum, dap->comm,
                                   static_cast<cudaStream_t>(stream)),

@@ -65,6 +65,7 @@ def load():
                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.c_int32, ctypes.c_void_p]
             L.evo_dap_barrier.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            L.evo_dap_wait.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double]
             L.evo_dap_init.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                        ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
             L.evo_dap_destroy.argtypes = [ctypes.c_void_p]
@@ -177,6 +178,12 @@ class NcclDap:
 
     def barrier(self, stream=None):
         _check(load().evo_dap_barrier(self.h, _p(self._scratch), _stream(stream)))
+
+    def wait(self, stream=None, timeout_s=300.0):
+        """Block until `stream` is idle while polling NCCL's asynchronous error state; a
+        peer failure or a hang longer than timeout_s aborts the communicator and raises
+        (evo_dap_wait, include/evo_dap.h)."""
+        _check(load().evo_dap_wait(self.h, _stream(stream), float(timeout_s)))
 
 
 # ----------------------------------------------------------------------------- shard plan

@@ -48,6 +48,7 @@ def run(args, metric):
 
     for _ in range(args.warmup):
         step()
+    comm.wait(stream)  # NCCL async-error polling with a timeout instead of a bare synchronize
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -87,6 +88,7 @@ def run(args, metric):
         else:
             step()
         ev[s][1].record(stream)
+    comm.wait(stream)
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     t = torch.tensor([ms], device=dev)

@@ -53,6 +53,36 @@ class GlooComm:
         return t[self.rank * h:(self.rank + 1) * h].contiguous()
 
 
+class PackA2AComm(GlooComm):
+    """The transpose exactly as libevodap performs it (csrc/evo_dap.cu,
+    evo_dap_alltoall_transpose): dir 0 packs the row shard [A/n][Bd][C] into [n][A/n][Bd/n·C]
+    (swap01 of [A/n][n][W] with W = Bd/n·C, the evo_dap_pack formula), one all-to-all of
+    equal contiguous blocks, and the received buffer IS the column shard [A][Bd/n][C] (no
+    unpack); dir 1 sends the column shard's contiguous row blocks as they are and unpacks
+    [n][A/n][W] -> [A/n][n][W].  Byte-level layout checked against GlooComm's gather/slice
+    semantics by running the whole block with it."""
+
+    @staticmethod
+    def _swap01(x, X, Y):  # [X][Y][W] -> [Y][X][W]: the evo_dap_pack kernel's mapping
+        return x.reshape(X, Y, -1).permute(1, 0, 2).contiguous()
+
+    def transpose(self, src, direction):
+        n = self.n
+        src = src.contiguous()
+        rest = tuple(src.shape[2:])
+        if direction == 0:
+            A_loc, Bd = src.shape[0], src.shape[1]
+            send = self._swap01(src, A_loc, n).reshape(-1)          # [n][A/n][W]
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send)
+            return recv.reshape((A_loc * n, Bd // n) + rest)       # [A][Bd/n][C], no unpack
+        A, W_loc = src.shape[0], src.shape[1]
+        send = src.reshape(-1)                                     # row blocks j·A/n.. -> rank j
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send)
+        return self._swap01(recv, n, A // n).reshape((A // n, W_loc * n) + rest)
+
+
 class OracleAttn:
     """The attention core's fwd/bwd signature on top of the fp64 oracle; outputs take the
     strides of the matching input, as the C ABI does."""
@@ -162,14 +192,14 @@ def _compare(got, ref, name):
     assert err < 1e-12, f"{name}: rel err {err:.3e}"
 
 
-def _worker(rank, n, port, mask, q):
+def _worker(rank, n, port, mask, q, comm_cls=GlooComm):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=n)
         oracle.set_num_threads(1)
         loc, full = dap.make_block_inputs(torch, n, rank, **SHAPE, seed=7, dtype=torch.float64,
                                           mask=mask)
-        blk = dap.DapEvoformerAttention(GlooComm(), OracleAttn(), loc)
+        blk = dap.DapEvoformerAttention(comm_cls(), OracleAttn(), loc)
         m_next, z_next, outs = blk.forward()
         grads = blk.backward(loc["dm_next"], loc["dz_next"])
         ref = unsharded_reference(full)
@@ -191,12 +221,17 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("n,mask", [(1, "ones"), (2, "ones"), (2, "prefix"), (4, "prefix")])
-def test_dap_block_matches_unsharded(n, mask):
+@pytest.mark.parametrize("n,mask,comm", [(1, "ones", "gather"), (2, "ones", "gather"),
+                                         (2, "prefix", "gather"), (4, "prefix", "gather"),
+                                         (2, "prefix", "pack_a2a"), (4, "prefix", "pack_a2a")])
+def test_dap_block_matches_unsharded(n, mask, comm):
+    """comm = "gather": the exchanges' reference semantics; "pack_a2a": the transposes as
+    libevodap lays them out (pack formula + one equal-block all-to-all, PackA2AComm)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, n, port, mask, q)) for r in range(n)]
+    cls = GlooComm if comm == "gather" else PackA2AComm
+    procs = [ctx.Process(target=_worker, args=(r, n, port, mask, q, cls)) for r in range(n)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(n))

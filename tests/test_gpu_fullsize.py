@@ -40,3 +40,29 @@ def test_bench_module_fullsize(idx):
             errs[n] = rel_err(_logical(r[n]), rg[n])
     bad = {k_: v_ for k_, v_ in errs.items() if not v_ <= TOL}
     assert not bad, f"{name}: {errs}"
+
+
+# BASELINE.json configs[3] and configs[4] at their full module sizes, prefix masks (the parity
+# recipe of DESIGN.md §4), every output element against the fp64 oracle (run_case):
+#   cfg 4  extra-MSA column attention: B = N_res = 256, H = 8, L = N_extra = 1024, D = 8, no bias,
+#          column layout (batch axis in the middle of the storage), 8 key tiles (dQ parts).
+#   cfg 5  N_res = 384 fine-tune crop (N_seq = 512, reading R12): triangle start / end with the
+#          shared pair bias (k- and q-contiguous) at L = 384 (the two-pass backward), and the
+#          MSA column attention B = 384, L = 512 (4 key tiles, no bias).
+FULL_CFGS = [
+    ("cfg4_extra_msa_col", dict(B=256, H=8, L=1024, D=8, bias=None, bias_t=False, layout="lbhd")),
+    ("cfg5_start", dict(B=384, H=4, L=384, D=32, bias="shared", bias_t=False, layout="blhd")),
+    ("cfg5_end", dict(B=384, H=4, L=384, D=32, bias="shared", bias_t=True, layout="lbhd")),
+    ("cfg5_col", dict(B=384, H=8, L=512, D=32, bias=None, bias_t=False, layout="lbhd")),
+]
+
+
+@pytest.mark.parametrize("cfg", FULL_CFGS, ids=[c[0] for c in FULL_CFGS])
+def test_fullsize_cfg4_cfg5(cfg):
+    from gpu_harness import run_case
+    name, p = cfg
+    errs, _, _ = run_case(p["B"], p["H"], p["L"], p["L"], p["D"], seed=11, bias=p["bias"],
+                          bias_t=p["bias_t"], mask="prefix", mask_t=p["layout"] == "lbhd",
+                          layout=p["layout"])
+    bad = {k_: v_ for k_, v_ in errs.items() if not v_ <= TOL}
+    assert not bad, f"{name}: {errs}"
