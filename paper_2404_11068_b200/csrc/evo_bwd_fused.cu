@@ -36,6 +36,18 @@
 
 namespace evo {
 
+#ifdef EVO_TIMELINE
+// Debug builds only (tools/timeline.py compiles a separate library with -DEVO_TIMELINE):
+// clock64 stamps of CTAs 0 and 1, 12 event kinds x 512 sub-tiles each.
+__device__ unsigned long long g_tl[2][12][512];
+#define TL(ev, i)                                                                \
+  do {                                                                           \
+    if (blockIdx.x < 2 && (i) < 512) g_tl[blockIdx.x][ev][i] = clock64();        \
+  } while (0)
+#else
+#define TL(ev, i) do { } while (0)
+#endif
+
 template <int DP, bool BIAS>
 struct FusedCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
@@ -170,6 +182,7 @@ __global__ void __launch_bounds__(384, 1)
         const int T = sbi * nq + stt, st = T & 1, kvs = sbi & 1;
         if (sss == 0) mbar_wait(bar_in + 8 * st, (T >> 1) & 1);
         if (sss == 0 && stt == 0) mbar_wait(bar_kv + 8 * kvs, (sbi >> 1) & 1);
+        TL(0, j);  // S/dP pair issued
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + sss * 32 * C::kRowBytes;
@@ -203,8 +216,10 @@ __global__ void __launch_bounds__(384, 1)
         const int g = i & 1;
         const int T = dbi * nq + dtt, st = T & 1, kvs = dbi & 1;
         mbar_wait(bar_ps + 8 * g, (i >> 1) & 1);
+        TL(4, i);  // hand-off seen by the grad issuer
         // the first sub-tile of a new batch row overwrites dK/dV: group 0 must have pulled them
         if (dtt == 0 && dss == 0 && dbi > 0) mbar_wait(bar_dkvfree, (dbi - 1) & 1);
+        TL(5, i);  // dV/dK issued
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
         const uint32_t ab = qb + C::kTile;
@@ -221,6 +236,7 @@ __global__ void __launch_bounds__(384, 1)
                     make_sdesc(qb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                     idesc_kv, (acc0 | (uint32_t)kk) ? 1u : 0u);
         umma_commit(bar_mm + 8 * g);
+        TL(8, i);  // dV/dK issue finished
         if (dss == 3) {  // the tile's 4 dSᵀ blocks are complete: dQ part = dS·K
           const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
 #pragma unroll
@@ -229,6 +245,7 @@ __global__ void __launch_bounds__(384, 1)
                       make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                       idesc_q, kk > 0 ? 1u : 0u);
           umma_commit(bar_dq + 8 * st);
+          TL(6, T);  // dQ issued
           // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the groups' hand-offs;
           // dV/dK/dQ: this thread) is done once these commits land
           umma_commit(bar_infree + 8 * st);
@@ -336,6 +353,7 @@ __global__ void __launch_bounds__(384, 1)
     // tile, else this key tile's fp32 part (dq_convert sums the parts); swizzled staging + TMA store
     auto drain_q = [&](int Tq) {
       mbar_wait(bar_dq + 8 * (Tq & 1), (Tq >> 1) & 1);
+      if (qd == 0 && lane == 0) TL(7, Tq);  // dQ landed (drain)
       tc_fence_after();
       if (lane == 0) bulk_wait_group_read0();
       __syncwarp();
@@ -393,7 +411,9 @@ __global__ void __launch_bounds__(384, 1)
         if ((bi & 31) == 0) keep_word = load_keep_word(b);
         keep = (keep_word >> (bi & 31)) & 1u;
       }
+      if (qd == 0 && lane == 0) TL(1, j);  // group starts waiting for S
       mbar_wait(bar_sp + 8 * g, (j >> 1) & 1);
+      if (qd == 0 && lane == 0) TL(2, j);  // S landed
       tc_fence_after();
       uint32_t rs[32], rd[32];
       const int qcol = t * 128 + s * 32;  // first query of this sub-tile
@@ -406,6 +426,7 @@ __global__ void __launch_bounds__(384, 1)
         if (BIAS && bi > 0) tmem_ld32(tDB + lane_base + qcol, acc);
       }
       tmem_wait_ld();
+      if (qd == 0 && lane == 0) TL(11, j);  // Sᵀ/dPᵀ/Σ in registers
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_sfree + 8 * g);
@@ -469,8 +490,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       // before overwriting: Pᵀ slot g is read by dV(j-2); this tile's dSᵀ buffer (T & 1) by tile
       // T-2's dQ MMA, long done (checked at the group's first sub-tile of a tile)
+      if (qd == 0 && lane == 0) TL(9, j);  // math + Σ store done
       if (j >= 2) mbar_wait(bar_mm + 8 * g, ((j - 2) >> 1) & 1);
       if (s == g && T >= 2) mbar_wait(bar_dq + 8 * st, ((T - 2) >> 1) & 1);
+      if (qd == 0 && lane == 0) TL(10, j);  // Pᵀ slot / dSᵀ buffer free
       tc_fence_after();
       // Pᵀ -> TMEM slot g (the A operand of the TS-form dV MMA); dSᵀ (block s) rows to smem:
       // this thread's key row, 32 queries = 4 x 16 B, SW64
@@ -486,6 +509,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_ps + 8 * g);
+      if (qd == 0 && lane == 0) TL(3, j);  // hand-off
       if (g == 0 && s == 0 && t == 0 && bi > 0) {
         // the previous row's last dV/dK MMAs were group 1's sub-tile j - 1 (bar_mm slot 1)
         mbar_wait(bar_mm + 8, ((j - 1) >> 1) & 1);
@@ -540,6 +564,13 @@ static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) 
                                           L.tm_b, L.args);
   return cudaGetLastError();
 }
+
+#ifdef EVO_TIMELINE
+extern "C" int evo_debug_timeline_copy(void* dst, size_t bytes) {
+  if (bytes > sizeof(g_tl)) bytes = sizeof(g_tl);
+  return (int)cudaMemcpyFromSymbol(dst, g_tl, bytes);
+}
+#endif
 
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {
 #define EVO_FUSED_CASE(dp, bb) \
