@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t my_cta_rank() {
   return r;
 }
 
-template <int N>
+template <int N, bool FRESH = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k2(unsigned long long* out, int n_mma) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -72,9 +72,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k2(unsigned 
   unsigned long long t0 = clock64();
   if (rank == 0 && threadIdx.x == 0) {
     constexpr uint32_t idesc = make_idesc_bf16(256, N, 0, 0);
-    const uint64_t ad = make_sdesc(s0, 16, 512, kSw64);
-    const uint64_t bd = make_sdesc(s0 + 65536, 16, 512, kSw64);
     for (int i = 0; i < n_mma; ++i) {
+      const int r = FRESH ? (i & 7) : 0;
+      const uint64_t ad = make_sdesc(s0 + r * 8192, 16, 512, kSw64);
+      const uint64_t bd = make_sdesc(s0 + 65536 + r * 4096, 16, 512, kSw64);
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
           "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm + (uint32_t)((i & 1) * N)),
@@ -126,5 +127,9 @@ int main() {
   run(k2<32>, "cta_group::2 M256 N32 (per SM)", 148, 1, 2.0 * 128 * 32 * 16);
   run(k2<64>, "cta_group::2 M256 N64 (per SM)", 148, 1, 2.0 * 128 * 64 * 16);
   run(k2<128>, "cta_group::2 M256 N128 (per SM)", 148, 1, 2.0 * 128 * 128 * 16);
+  run(k2<32, true>, "cta_group::2 M256 N32 fresh", 148, 1, 2.0 * 128 * 32 * 16);
+  run(k2<64, true>, "cta_group::2 M256 N64 fresh", 148, 1, 2.0 * 128 * 64 * 16);
+  run(k2<128, true>, "cta_group::2 M256 N128 fresh", 148, 1, 2.0 * 128 * 128 * 16);
+  run(k2<256, true>, "cta_group::2 M256 N256 fresh", 148, 1, 2.0 * 128 * 256 * 16);
   return 0;
 }
