@@ -317,14 +317,34 @@ def run_gpu(args):
         mods.append((name, B, H, L, bias, t, ws))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
+    # The block's two attention stacks are independent (MSA: row -> col; pair: start -> end):
+    # the pair stack runs on a second stream so its kernels fill the SMs the MSA stack's leave
+    # idle (kernel tails, low-occupancy phases) — the same overlap the DAP block uses.
+    pair_stream = None if args.no_overlap else torch.cuda.Stream()
+
+    def run_mod(name, B, H, L, bias, t, ws):
+        o, lse = evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
+        n = evoattn.last_launch_count()
+        evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"], t["mask"], t["g"],
+                    workspace=ws)
+        return n + evoattn.last_launch_count()
+
+    def step(overlap=True):
         launches = 0
-        for name, B, H, L, bias, t, ws in mods:
-            o, lse = evoattn.fwd(t["q"], t["k"], t["v"], t["bias"], t["mask"], t["g"])
-            launches += evoattn.last_launch_count()
-            evoattn.bwd(t["q"], t["k"], t["v"], o, lse, t["dout"], t["bias"], t["mask"], t["g"],
-                        workspace=ws)
-            launches += evoattn.last_launch_count()
+        if pair_stream is None or not overlap:
+            for m in mods:
+                launches += run_mod(*m)
+            return launches
+        main = torch.cuda.current_stream()
+        pair_stream.wait_stream(main)
+        with torch.cuda.stream(pair_stream):
+            for m in mods:
+                if m[0] in ("start", "end"):
+                    launches += run_mod(*m)
+        for m in mods:
+            if m[0] in ("row", "col"):
+                launches += run_mod(*m)
+        main.wait_stream(pair_stream)
         return launches
 
     for _ in range(args.warmup):
@@ -377,10 +397,10 @@ def run_gpu(args):
     torch.cuda.synchronize()
     trace_arr = (__import__("ctypes").c_void_p * len(trace_ev))(*[e.cuda_event for e in trace_ev])
     lib.evo_trace_enable(trace_arr, len(trace_ev))
-    for s in range(args.steps):
+    for s in range(args.steps):  # one stream here: each kernel's own duration, not a share
         if not args.no_flush:
             flush.zero_()
-        step()
+        step(overlap=False)
     torch.cuda.synchronize()
     ntr = lib.evo_trace_count()
     labels = [lib.evo_trace_label(i).decode() for i in range(ntr)]
@@ -401,6 +421,17 @@ def run_gpu(args):
     cpu = cpu_baseline(args.cpu_seconds) if not args.no_cpu else None
     configs = None if args.no_configs else run_configs(
         torch, evoattn, dev, flush, max(3, min(args.steps, 10)), clk.get("sm_mhz"))
+    stack = None
+    if args.stack_blocks > 0:  # §8(f) f4: a chained stack of DAP blocks under one CUDA graph
+        from paper_2404_11068_b200 import dap, dap_bench
+        comm = dap.NcclDap()
+        pair = None if args.no_overlap else (dap.NcclDap(store_key="evo_dap_uid_pair"),
+                                              torch.cuda.Stream())
+        stack = dap_bench.run_stack(torch, None, dap, evoattn, comm, pair, 1, 0, dev,
+                                    args.stack_nseq, args.stack_nres, args.stack_blocks, args)
+        if pair is not None:
+            pair[0].close()
+        comm.close()
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -412,7 +443,10 @@ def run_gpu(args):
                    "l2": "flushed (256 MB write) before every timed step" if not args.no_flush
                    else "warm", "parallelism": "single GPU",
                    "launch": "CUDA graph of the step" if graph is not None else "eager",
-                   "kernel_timing": "per-launch CUDA events over K further eager steps"},
+                   "streams": "MSA stack (row, col) and pair stack (start, end) on two streams"
+                   if pair_stream is not None else "one stream",
+                   "kernel_timing": "per-launch CUDA events over K further eager steps (one "
+                                    "stream)"},
         "pct_of_peak": {"tensor_measured": value / measured_peaks()["bf16_tflops"],
                         "tensor_nominal": value / 2250.0},
         "roofline": roof,
@@ -422,6 +456,7 @@ def run_gpu(args):
         "gpu_launches": launches,
         "cpu_baseline": cpu,
         "configs": configs,
+        "stack": stack,
     }
     print(json.dumps(line), flush=True)
 
@@ -667,6 +702,12 @@ def main():
     ap.add_argument("--dap", action="store_true", help="run the DAP path even at N=1")
     ap.add_argument("--nseq", type=int, default=None, help="(DAP) override N_seq")
     ap.add_argument("--nres", type=int, default=None, help="(DAP) override N_res")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="(DAP) run the pair stack on the caller's stream (no overlap)")
+    ap.add_argument("--stack-blocks", type=int, default=8,
+                    help="blocks of the chained DAP stack timed under one CUDA graph (0: skip)")
+    ap.add_argument("--stack-nres", type=int, default=384)
+    ap.add_argument("--stack-nseq", type=int, default=512)
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -24,6 +24,22 @@
 
 namespace evo {
 
+#ifdef EVO_TIMELINE
+// Debug builds only (tools/fwd_timeline.py): per CTA (first 4096) its SM id and clock64 stamps:
+// [0] start, [1] Q row in TMEM, [2 + 2c] S_c landed, [3 + 2c] P_c written (c < 8), [18] end.
+__device__ unsigned long long g_ftl[4096][20];
+#define FTL(i)                                                                   \
+  do {                                                                           \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_ftl[blockIdx.x][i] = clock64(); \
+  } while (0)
+extern "C" int evo_debug_fwd_timeline_copy(void* dst, size_t bytes) {
+  if (bytes > sizeof(g_ftl)) bytes = sizeof(g_ftl);
+  return (int)cudaMemcpyFromSymbol(dst, g_ftl, bytes);
+}
+#else
+#define FTL(i) do { } while (0)
+#endif
+
 template <int DP, int BIAS>
 struct OccCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
@@ -64,6 +80,14 @@ __global__ void __launch_bounds__(128, 4)
   const int h = bh % a.H, b = bh / a.H;
   const int q0 = qt * 128, q = q0 + tid;
   const bool qv = q < a.Lq;
+#ifdef EVO_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_ftl[blockIdx.x][19] = smid;
+  }
+#endif
+  FTL(0);
 
   if (w == 0) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -176,6 +200,7 @@ __global__ void __launch_bounds__(128, 4)
   tmem_wait_st();
   tc_fence_before();
   __syncthreads();  // Q in TMEM, mask words in smem
+  FTL(1);
   if (tid == 0) {
     tc_fence_after();
     mbar_wait(bar_kv0, 0);
@@ -191,6 +216,7 @@ __global__ void __launch_bounds__(128, 4)
     uint32_t mw0 = ~0u, mw1 = ~0u;
     if (!all_kept) { mw0 = smask[2 * c]; mw1 = smask[2 * c + 1]; }
     mbar_wait(bar_s, c & 1);
+    if (c < 8) FTL(2 + 2 * c);
     tc_fence_after();
     if (tid == 0 && c >= 1 && c - 1 + C::kNSt < nc) {
       // PV_{c-1} has landed (it precedes S_c in the MMA pipe): chunk c-1's stage is free
@@ -289,6 +315,7 @@ __global__ void __launch_bounds__(128, 4)
     }
     tmem_st32(tS + lane_base, pk);  // P over the consumed S columns [0, 32)
     tmem_wait_st();
+    if (c < 8) FTL(3 + 2 * c);
     tc_fence_before();
     __syncthreads();  // all P written; S_c fully consumed; bias stage read
     if (tid == 0) {
@@ -372,6 +399,7 @@ __global__ void __launch_bounds__(128, 4)
     a.lse[((int64_t)b * a.H + h) * a.Lq + q] =
         l_run > 0.f ? (m_ref == -INFINITY ? 0.f : m_ref) + __logf(l_run) : -INFINITY;
   }
+  FTL(18);
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<C::kTmemCols>(tmem);

@@ -97,6 +97,20 @@ def pack(src, dst, n, A_loc, Bd, C_bytes, direction, stream=None):
                                _stream(stream)))
 
 
+class _stdout_to_stderr:
+    """Redirect the process-level stdout (fd 1) to stderr for the duration of a native call."""
+
+    def __enter__(self):
+        import sys
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 class NcclDap:
     """One NCCL communicator over the torch.distributed world (include/evo_dap.h).  The NCCL
     unique id travels over the torch.distributed store."""
@@ -116,7 +130,8 @@ class NcclDap:
             dist.broadcast_object_list(obj, src=0)
             uid = ctypes.create_string_buffer(obj[0], 128)
         h = ctypes.c_void_p()
-        _check(L.evo_dap_init(self.n, self.rank, uid, self.device, ctypes.byref(h)))
+        with _stdout_to_stderr():  # NCCL's init banner must not land in a JSON-line stdout
+            _check(L.evo_dap_init(self.n, self.rank, uid, self.device, ctypes.byref(h)))
         self.h = h
         self._scratch = torch.zeros(4, dtype=torch.float32, device="cuda")
         self._staging = None
@@ -227,13 +242,38 @@ class DapEvoformerAttention:
     backward(dm_next, dz_next) returns every input gradient on its shard (dbias shards fp32).
     """
 
-    def __init__(self, comm, attn, inputs):
+    def __init__(self, comm, attn, inputs, pair=None):
+        """pair = (comm2, stream): run the pair stack (triangle start/end and their exchanges)
+        on `stream` with its own communicator while the MSA stack runs on the caller's stream
+        (one stack's collectives overlap the other's attention); the two
+        stacks of the attention core are independent inside a block.  None: one stream."""
         self.comm, self.attn, self.x = comm, attn, inputs
         self.n, self.rank = comm.n, comm.rank
+        self.pair = pair
+
+    def _fork(self):
+        """-> (pair-stack comm, stream context, join()): fork the pair stack onto its stream."""
+        import contextlib
+        if self.pair is None:
+            return self.comm, contextlib.nullcontext(), (lambda *outs: None)
+        import torch
+        comm2, st2 = self.pair
+        main = torch.cuda.current_stream()
+        st2.wait_stream(main)
+
+        def join(*outs):
+            main.wait_stream(st2)
+            for t in outs:  # produced on the pair stream, consumed on the caller's
+                if t is not None:
+                    t.record_stream(main)
+        return comm2, torch.cuda.stream(st2), join
 
     def forward(self):
         x, c = self.x, self.comm
         s = {}
+        cz, ctx, join = self._fork()
+        with ctx:
+            z_next = self._forward_pair(x, cz, s)
         # MSA stack: bias AG -> row attention -> a2a (S -> R) -> column attention -> a2a back
         s["E_row"] = c.allgather(x["E_row"])
         o_row, o_row_v, s["lse_row"] = M.attention_fwd("row", x["row_q"], x["row_k"], x["row_v"],
@@ -246,6 +286,12 @@ class DapEvoformerAttention:
                                                             x["col_g"], None, x["mask_col"],
                                                             self.attn)
         m_next = c.transpose(o_col.reshape(o_col.shape[0], o_col.shape[1], Hm * D), 1)
+        join(z_next, s["o_st"], s["o_end"])
+        self.saved = s
+        return m_next, z_next, {"o_row": o_row, "o_col": o_col, "o_start": s["o_st"],
+                                "o_end": s["o_end"]}
+
+    def _forward_pair(self, x, c, s):
         # pair stack: bias AG -> triangle start -> a2a (I -> J) -> triangle end -> a2a back
         s["E_start"] = c.allgather(x["E_start"])
         o_st, s["o_st_v"], s["lse_st"] = M.attention_fwd("start", x["st_q"], x["st_k"], x["st_v"],
@@ -258,12 +304,20 @@ class DapEvoformerAttention:
                                                             x["end_g"], s["E_end"], x["mask_end"],
                                                             self.attn)
         z_next = c.transpose(o_end.reshape(o_end.shape[0], o_end.shape[1], Hz * Dz), 1)
-        self.saved = s
-        return m_next, z_next, {"o_row": o_row, "o_col": o_col, "o_start": o_st, "o_end": o_end}
+        s["o_st"], s["o_end"] = o_st, o_end
+        return z_next
 
     def backward(self, dm_next, dz_next):
         x, c, s = self.x, self.comm, self.saved
         g = {}
+        cz, ctx, join = self._fork()
+        with ctx:
+            self._backward_pair(x, cz, s, g, dz_next)
+        self._backward_msa(x, c, s, g, dm_next)
+        join(*g.values())
+        return g
+
+    def _backward_pair(self, x, c, s, g, dz_next):
         # pair stack, reversed: dz (I-sharded) -> J-sharded -> end bwd -> RS(dE_end); dq_end -> I
         Hz, Dz = x["st_q"].shape[2], x["st_q"].shape[3]
         d_end = c.transpose(dz_next.contiguous(), 0)
@@ -279,6 +333,8 @@ class DapEvoformerAttention:
                             x["mask_start"], s["o_st_v"], s["lse_st"], d_st, self.attn)
         g["st_q"], g["st_k"], g["st_v"], g["st_g"] = r["dq"], r["dk"], r["dv"], r["dg"]
         g["E_start"] = c.reduce_scatter(_dense(r["dE"]))
+
+    def _backward_msa(self, x, c, s, g, dm_next):
         # MSA stack, reversed: dm (S-sharded) -> R-sharded -> col bwd; dq_col -> S -> row bwd
         Hm, D = x["row_q"].shape[2], x["row_q"].shape[3]
         d_col = c.transpose(dm_next.contiguous(), 0)
@@ -293,7 +349,41 @@ class DapEvoformerAttention:
                             x["mask_row"], s["o_row_v"], s["lse_row"], d_row, self.attn)
         g["row_q"], g["row_k"], g["row_v"], g["row_g"] = r["dq"], r["dk"], r["dv"], r["dg"]
         g["E_row"] = c.reduce_scatter(_dense(r["dE"]))
-        return g
+
+
+class DapEvoformerStack:
+    """`n_blocks` Evoformer blocks' attention cores chained (PAPER.md L264 / SURVEY §8(f) f4: the
+    48-block stack under one CUDA graph): block i+1's MSA-row query is block i's m_next and its
+    triangle-start query is block i's z_next (the projections between blocks are outside the
+    attention core); the backward chains dm/dz back through the blocks.  The per-block k, v, g,
+    bias and mask tensors are shared by every block (synthetic inputs; the timing is the same as
+    with distinct tensors of the same shapes)."""
+
+    def __init__(self, comm, attn, inputs, n_blocks, pair=None):
+        self.blocks = []
+        self.x0 = inputs
+        for _ in range(n_blocks):
+            self.blocks.append(DapEvoformerAttention(comm, attn, dict(inputs), pair))
+
+    def forward(self):
+        m, z = None, None
+        for i, blk in enumerate(self.blocks):
+            if i > 0:
+                S_loc, R, _ = m.shape
+                blk.x["row_q"] = m.view(S_loc, R, *self.x0["row_q"].shape[2:])
+                I_loc, J, _ = z.shape
+                blk.x["st_q"] = z.view(I_loc, J, *self.x0["st_q"].shape[2:])
+            m, z, _ = blk.forward()
+        return m, z
+
+    def backward(self, dm_next, dz_next):
+        dm, dz = dm_next, dz_next
+        g = None
+        for blk in reversed(self.blocks):
+            g = blk.backward(dm, dz)
+            dm = g["row_q"].reshape(g["row_q"].shape[0], g["row_q"].shape[1], -1)
+            dz = g["st_q"].reshape(g["st_q"].shape[0], g["st_q"].shape[1], -1)
+        return dm, dz, g
 
 
 def _dense(t):

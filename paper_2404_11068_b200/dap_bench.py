@@ -36,9 +36,13 @@ def run(args, metric):
     n_seq = args.nseq or 128
     n_res = args.nres or 256
     comm = dap.NcclDap()
+    # the pair stack on its own stream and communicator, overlapping the MSA stack (§8(e))
+    pair = None
+    if not getattr(args, "no_overlap", False):
+        pair = (dap.NcclDap(store_key="evo_dap_uid_pair"), torch.cuda.Stream())
     loc, _ = dap.make_block_inputs(torch, world, rank, n_seq, n_res, seed=0, device=dev)
     attn = _Counting(evoattn)
-    blk = dap.DapEvoformerAttention(comm, attn, loc)
+    blk = dap.DapEvoformerAttention(comm, attn, loc, pair)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -143,8 +147,17 @@ def run(args, metric):
             "kernels": kernels,
             "e2e": e2e,
             "gpu_launches": launches,
+            "overlap": "pair stack on its own stream + communicator" if pair else "none",
         }
+    stack = None
+    if getattr(args, "stack_blocks", 0) > 0:
+        stack = run_stack(torch, dist, dap, evoattn, comm, pair, world, rank, dev,
+                          args.stack_nseq, args.stack_nres, args.stack_blocks, args)
+    if rank == 0:
+        line["stack"] = stack
         print(json.dumps(line), flush=True)
+    if pair is not None:
+        pair[0].close()
     comm.close()
     if world > 1:
         dist.barrier()
@@ -166,6 +179,63 @@ class _Counting:
         r = self.mod.bwd(*a, **k)
         self.launches += self.mod.last_launch_count()
         return r
+
+
+def run_stack(torch, dist, dap, evoattn, comm, pair, world, rank, dev, n_seq, n_res, blocks,
+              args):
+    """`blocks` chained Evoformer attention-core blocks (fwd through the stack,
+    then bwd back) under DAP-`world`, captured as ONE CUDA graph and replayed; device time per
+    replay (CUDA events, max over ranks), L2 flushed before each.  Returns ms per stack and per
+    block plus the algorithmic TFLOP/s."""
+    import numpy as np
+    loc, _ = dap.make_block_inputs(torch, world, rank, n_seq, n_res, seed=1, device=dev)
+    st = dap.DapEvoformerStack(comm, evoattn, loc, blocks, pair)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        st.forward()
+        return st.backward(loc["dm_next"], loc["dz_next"])
+
+    step()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    reps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    for a, b in ev:
+        flush.zero_()
+        comm.barrier()
+        a.record(stream)
+        graph.replay()
+        b.record(stream)
+    comm.wait(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    fl = blocks * dap.block_flops(n_seq, n_res)
+    del graph, st
+    torch.cuda.empty_cache()
+    return {"blocks": blocks, "n_res": n_res, "n_seq": n_seq, "parallelism": f"dap{world}",
+            "launch": "one CUDA graph of the whole stack (fwd + bwd)", "ms_per_stack": ms,
+            "ms_per_block": ms / blocks, "ms_per_48_blocks": 48 * ms / blocks,
+            "tflops_alg": fl / (ms * 1e-3) / 1e12, "replays": reps,
+            "l2": "flushed before each replay",
+            "note": "per-block k/v/g/bias tensors shared across blocks; q chained m_next/z_next"}
 
 
 def _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops):

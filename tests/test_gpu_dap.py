@@ -67,3 +67,48 @@ def test_dap_block_world1_matches_oracle():
         err = (a - r).norm() / max(r.norm(), 1e-30)  # normwise relative
         assert err < 2e-2, f"{name}: {err:.3e}"
     comm.close()
+
+
+def test_dap_block_overlap_is_bitwise_identical():
+    """The pair stack on its own stream + communicator (overlapping the MSA stack) changes no
+    output bit of the block's forward or backward (same kernels, same inputs, §5b orders)."""
+    shape = dict(n_seq=32, n_res=64, heads_m=8, heads_z=4, head_dim=32)
+    loc, _ = dap.make_block_inputs(torch, 1, 0, **shape, seed=4, device="cuda", mask="prefix")
+    comm = dap.NcclDap()
+    comm2 = dap.NcclDap(store_key="evo_dap_uid_pair")
+    outs = []
+    for pair in (None, (comm2, torch.cuda.Stream())):
+        blk = dap.DapEvoformerAttention(comm, evoattn, dict(loc), pair)
+        m_next, z_next, _ = blk.forward()
+        g = blk.backward(loc["dm_next"], loc["dz_next"])
+        comm.wait(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        outs.append(dict(g, m_next=m_next, z_next=z_next))
+    for k, v in outs[0].items():
+        if v is not None:
+            assert torch.equal(v, outs[1][k]), k
+    comm2.close()
+    comm.close()
+
+
+def test_dap_stack_chains_blocks():
+    """DapEvoformerStack: block 2's queries are block 1's outputs (m_next, z_next), and the
+    backward chains dm/dz back — checked against two explicitly chained blocks."""
+    shape = dict(n_seq=16, n_res=32, heads_m=8, heads_z=4, head_dim=32)
+    loc, _ = dap.make_block_inputs(torch, 1, 0, **shape, seed=5, device="cuda")
+    comm = dap.NcclDap()
+    st = dap.DapEvoformerStack(comm, evoattn, loc, 2, None)
+    m, z = st.forward()
+    dm, dz, _ = st.backward(loc["dm_next"], loc["dz_next"])
+    b1 = dap.DapEvoformerAttention(comm, evoattn, dict(loc))
+    m1, z1, _ = b1.forward()
+    x2 = dict(loc, row_q=m1.view(loc["row_q"].shape), st_q=z1.view(loc["st_q"].shape))
+    b2 = dap.DapEvoformerAttention(comm, evoattn, x2)
+    m2, z2, _ = b2.forward()
+    g2 = b2.backward(loc["dm_next"], loc["dz_next"])
+    g1 = b1.backward(g2["row_q"].reshape(m1.shape), g2["st_q"].reshape(z1.shape))
+    torch.cuda.synchronize()
+    assert torch.equal(m, m2) and torch.equal(z, z2)
+    assert torch.equal(dm, g1["row_q"].reshape(dm.shape))
+    assert torch.equal(dz, g1["st_q"].reshape(dz.shape))
+    comm.close()
