@@ -584,9 +584,21 @@ def run_side_paths(torch, evoattn, dev, flush, reps, pk):
             f()
         tf = _timed(torch, f, flush, reps)
         byt = rows * C * 2 + rows * N * 2 + N * C * 2 + rows * 8
+        # backward (dgrad + LN backward, wgrad, dγ/dβ/db): reads x, dout, W, mean/rstd; writes
+        # dx (bf16), dW (fp32); 2 GEMMs of 2·rows·C·N flops each
+        _, mean, rstd = evoattn.ln_proj_fwd(x, g, bt, W, bb)
+        dout = torch.randn((rows, N), device=dev).to(torch.bfloat16)
+        wsb = torch.empty(1 << 26, dtype=torch.uint8, device=dev)
+        fb = lambda: evoattn.ln_proj_bwd(x, g, bt, W, mean, rstd, dout, workspace=wsb)
+        for _ in range(3):
+            fb()
+        tb = _timed(torch, fb, flush, reps)
+        byb = rows * C * 2 * 2 + rows * N * 2 + N * C * 2 + N * C * 4 + rows * 8
         out[f"f2_ln_qkvg_proj_{name}_{rows}x{C}to{N}"] = {
             "fwd_ms": tf, "tflops": 2.0 * rows * C * N / (tf * 1e-3) / 1e12,
-            "hbm_frac": byt / (tf * 1e-3) / 1e9 / pk["hbm_gbs"]}
+            "hbm_frac": byt / (tf * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "bwd_ms": tb, "bwd_tflops": 4.0 * rows * C * N / (tb * 1e-3) / 1e12,
+            "bwd_hbm_frac": byb / (tb * 1e-3) / 1e9 / pk["hbm_gbs"]}
     B, S, H, D = 256, 1024, 8, 8
     gq = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)
     gg = torch.randn((S, B, H, D), device=dev).to(torch.bfloat16).transpose(0, 1)

@@ -56,6 +56,34 @@ evo_status_t evo_ln_proj_fwd(const evo_ln_proj_desc_t* d, const void* x, const f
 evo_status_t evo_linear_fwd(const evo_ln_proj_desc_t* d, const void* x, const void* W,
                             const float* b, void* out, void* stream);
 
+/* Backward of evo_ln_proj_fwd (the chain rule through PAPER.md L273's fused
+ * LayerNorm + four GEMMs).  Given dout = ∂L/∂out [rows][N] bf16 (row stride d->out_ld):
+ *
+ *   dy[r,c]  = Σ_n dout[r,n]·W[n,c]                                     (fp32, tcgen05)
+ *   x̂[r,c]  = (x[r,c] − mean_r)·rstd_r                                 (mean, rstd: the forward's)
+ *   dx[r,c]  = bf16( rstd_r·( dy·γ − (1/C)Σ_c dy·γ − x̂·(1/C)Σ_c dy·γ·x̂ ) )   row stride d->x_ld
+ *   dγ[c]    = Σ_r dy[r,c]·x̂[r,c],   dβ[c] = Σ_r dy[r,c]                 (fp32 [C])
+ *   dW[n,c]  = Σ_r dout[r,n]·y[r,c],  y = bf16(x̂·γ + β) (the forward's MMA operand)   (fp32 [N][C])
+ *   db[n]    = Σ_r dout[r,n]                                             (fp32 [N], skipped if NULL)
+ *
+ * Every sum over rows is taken in a fixed order (bitwise repeatable).  `dx` is written, never read;
+ * x, W, mean, rstd and dout are read only.  Workspace: evo_ln_proj_bwd_workspace_bytes(d) bytes of
+ * device memory, 16-byte aligned, owned by the caller (partials of dγ/dβ, dW and db).
+ * Supported: C in {64, 128, 256}; N a multiple of 128 (<= 2048).  Same alignment, error and
+ * stream conventions as evo_ln_proj_fwd. */
+size_t evo_ln_proj_bwd_workspace_bytes(const evo_ln_proj_desc_t* d);
+evo_status_t evo_ln_proj_bwd(const evo_ln_proj_desc_t* d, const void* x, const float* gamma,
+                             const float* beta, const void* W, const float* mean,
+                             const float* rstd, const void* dout, void* dx, float* dgamma,
+                             float* dbeta, float* dW, float* db, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Backward of evo_linear_fwd (no LayerNorm): dx = bf16(dout·W), dW = doutᵀ·x, db = Σ_r dout.
+ * Same layouts, workspace query (evo_ln_proj_bwd_workspace_bytes) and conventions. */
+evo_status_t evo_linear_bwd(const evo_ln_proj_desc_t* d, const void* x, const void* W,
+                            const void* dout, void* dx, float* dW, float* db, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

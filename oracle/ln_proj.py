@@ -35,3 +35,35 @@ def linear_fwd(x, W, b=None):
     if b is not None:
         out = out + np.asarray(b, np.float64)
     return out
+
+
+def ln_proj_bwd(x, gamma, beta, W, dout, eps=1e-5, ln=True):
+    """fp64 backward of out = LN(x)·Wᵀ + b (ln=True) or out = x·Wᵀ + b (ln=False), written from
+    the chain rule in the order of the forward (the LayerNorm backward of
+    [ext] Ba et al., as the paper's fused LN + GEMMs need it):
+      dy = dout·W;  dW = doutᵀ·y;  db = Σ_r dout
+      LN:  x̂ = (x − μ)/sqrt(σ² + eps),  dγ = Σ_r dy⊙x̂,  dβ = Σ_r dy,
+           g = dy⊙γ,  dx = (g − mean_c(g) − x̂·mean_c(g⊙x̂)) / sqrt(σ² + eps)
+    x [rows, C]; W [N, C] (nn.Linear layout); dout [rows, N].  Returns dict dx, dgamma, dbeta,
+    dW, db (dgamma/dbeta None without LN)."""
+    x = np.asarray(x, np.float64)
+    W = np.asarray(W, np.float64)
+    dout = np.asarray(dout, np.float64)
+    if ln:
+        mean = x.mean(axis=1, keepdims=True)
+        var = ((x - mean) ** 2).mean(axis=1, keepdims=True)
+        rstd = 1.0 / np.sqrt(var + eps)
+        xh = (x - mean) * rstd
+        y = xh * np.asarray(gamma, np.float64) + np.asarray(beta, np.float64)
+    else:
+        y = x
+    dy = dout @ W
+    out = {"dW": dout.T @ y, "db": dout.sum(axis=0), "dgamma": None, "dbeta": None}
+    if ln:
+        out["dgamma"] = (dy * xh).sum(axis=0)
+        out["dbeta"] = dy.sum(axis=0)
+        g = dy * np.asarray(gamma, np.float64)
+        out["dx"] = (g - g.mean(axis=1, keepdims=True) - xh * (g * xh).mean(axis=1, keepdims=True)) * rstd
+    else:
+        out["dx"] = dy
+    return out

@@ -130,6 +130,12 @@ def load():
             lib.evo_ln_proj_fwd.restype = i32
             lib.evo_linear_fwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 5
             lib.evo_linear_fwd.restype = i32
+            lib.evo_ln_proj_bwd_workspace_bytes.argtypes = [ctypes.POINTER(LnProjDesc)]
+            lib.evo_ln_proj_bwd_workspace_bytes.restype = sz
+            lib.evo_ln_proj_bwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 13 + [sz, vp]
+            lib.evo_ln_proj_bwd.restype = i32
+            lib.evo_linear_bwd.argtypes = [ctypes.POINTER(LnProjDesc)] + [vp] * 7 + [sz, vp]
+            lib.evo_linear_bwd.restype = i32
             _lib = lib
     return _lib
 
@@ -419,3 +425,47 @@ def linear_fwd(x, W, b=None, out=None, stream=None):
     _check(load().evo_linear_fwd(ctypes.byref(d), _ptr(x), _ptr(W.contiguous()), _ptr(b),
                                  _ptr(out), _stream(stream)))
     return out
+
+
+def ln_proj_bwd(x, gamma, beta, W, mean, rstd, dout, eps=1e-5, want_db=True, workspace=None,
+                stream=None):
+    """Backward of ln_proj_fwd (include/evo_ln_proj.h evo_ln_proj_bwd): dout [rows, N] bf16 ->
+    dict dx [rows, C] bf16, dgamma, dbeta [C] fp32, dW [N, C] fp32, db [N] fp32 (or None)."""
+    rows, C = x.shape
+    N = W.shape[0]
+    dx = torch.empty((rows, C), dtype=torch.bfloat16, device=x.device)
+    dgamma = torch.empty(C, dtype=torch.float32, device=x.device)
+    dbeta = torch.empty(C, dtype=torch.float32, device=x.device)
+    dW = torch.empty((N, C), dtype=torch.float32, device=x.device)
+    db = torch.empty(N, dtype=torch.float32, device=x.device) if want_db else None
+    d = LnProjDesc()
+    d.rows, d.C, d.N, d.eps = rows, C, N, eps
+    d.x_ld, d.out_ld = x.stride(0), dout.stride(0)
+    L = load()
+    need = int(L.evo_ln_proj_bwd_workspace_bytes(ctypes.byref(d)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    _check(L.evo_ln_proj_bwd(ctypes.byref(d), _ptr(x), _ptr(gamma), _ptr(beta),
+                             _ptr(W.contiguous()), _ptr(mean), _ptr(rstd), _ptr(dout), _ptr(dx),
+                             _ptr(dgamma), _ptr(dbeta), _ptr(dW), _ptr(db), _ptr(workspace), need,
+                             _stream(stream)))
+    return {"dx": dx, "dgamma": dgamma, "dbeta": dbeta, "dW": dW, "db": db}
+
+
+def linear_bwd(x, W, dout, want_db=True, workspace=None, stream=None):
+    """Backward of linear_fwd (evo_linear_bwd): dx = dout·W (bf16), dW = doutᵀ·x, db."""
+    rows, C = x.shape
+    N = W.shape[0]
+    dx = torch.empty((rows, C), dtype=torch.bfloat16, device=x.device)
+    dW = torch.empty((N, C), dtype=torch.float32, device=x.device)
+    db = torch.empty(N, dtype=torch.float32, device=x.device) if want_db else None
+    d = LnProjDesc()
+    d.rows, d.C, d.N, d.eps = rows, C, N, 0.0
+    d.x_ld, d.out_ld = x.stride(0), dout.stride(0)
+    L = load()
+    need = int(L.evo_ln_proj_bwd_workspace_bytes(ctypes.byref(d)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    _check(L.evo_linear_bwd(ctypes.byref(d), _ptr(x), _ptr(W.contiguous()), _ptr(dout), _ptr(dx),
+                            _ptr(dW), _ptr(db), _ptr(workspace), need, _stream(stream)))
+    return {"dx": dx, "dW": dW, "db": db}
