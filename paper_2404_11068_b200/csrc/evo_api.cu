@@ -551,10 +551,21 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.dq_reduce = dq_red ? 1 : 0;
     fa.bmode = bm;
     memset(&F.tm_b, 0, sizeof(F.tm_b));
-    if (bm && !make_bias_map(&F.tm_b, d, bias, bm == 1 ? 256 : 128))
+    // 256 < Lq <= 384 with a bias ("big"): the k-contiguous biasᵀ prologue stages 128 queries
+    // at a time, and a Σ-only second pass covers the query tile beyond 256
+    const bool big = bm && ((d->Lq + 127) / 128) * 128 > 256;
+    if (bm && !make_bias_map(&F.tm_b, d, bias, bm == 1 ? (big ? 128 : 256) : 128))
       return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for the fused backward's bias map");
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
+    fa.t0 = 0;
+    fa.sigma_only = 0;
     if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
+    if (big) {
+      ++nl;
+      fa.t0 = 2;
+      fa.sigma_only = 1;
+      if ((e = traced(st, "bwd_fused_sigma", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), 1, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused (sigma pass)");
+    }
     ++nl;
     // fork: the dbias reduce runs on the side stream while dq_convert runs on the caller's
     SideStream* ss = (dqacc && bm) ? side_stream() : nullptr;

@@ -48,16 +48,21 @@ __device__ unsigned long long g_tl[2][12][512];
 #define TL(ev, i) do { } while (0)
 #endif
 
-template <int DP, bool BIAS>
+// BIG: a shared bias with 256 < Lq <= 384 (BASELINE cfg 5, N_res = 384): the resident biasᵀ
+// grows to [128 k][384 q] and the dSᵀ blocks are single-buffered to stay inside 227 KB of smem;
+// Σ_b dSᵀ stays in TMEM for the first 256 queries (the main pass) and the remaining query tile
+// gets its own Σ-only pass (a.sigma_only, first tile a.t0 = 2).
+template <int DP, bool BIAS, bool BIG = false>
 struct FusedCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
   static constexpr uint32_t kTile = 128 * kRowBytes;  // one 128-row Q/K/V/dA tile
-  static constexpr uint32_t kBiasMax = BIAS ? 128u * 256u * 2u : 0u;
+  static constexpr uint32_t kBiasMax = BIAS ? 128u * (BIG ? 384u : 256u) * 2u : 0u;
+  static constexpr uint32_t kDS = BIG ? 32768u : 65536u;  // dSᵀ: (1 or 2) x 4 x 8 KB
   static constexpr uint32_t oBias = 0;
   static constexpr uint32_t oKV = oBias + kBiasMax;      // stage s: K at +s*2*kTile, V +kTile
   static constexpr uint32_t oQA = oKV + 4 * kTile;       // stage s: Q at +s*2*kTile, dA +kTile
-  static constexpr uint32_t oDS = oQA + 4 * kTile;       // 2 x 4 x 8 KB (tile T in buffer T & 1)
-  static constexpr uint32_t oVec = oDS + 65536;          // 2 x (lse2[128], D[128]) fp32
+  static constexpr uint32_t oDS = oQA + 4 * kTile;       // tile T in buffer BIG ? 0 : T & 1
+  static constexpr uint32_t oVec = oDS + kDS;            // 2 x (lse2[128], D[128]) fp32
   static constexpr uint32_t oStK = oVec + 2048;          // staging: dK, dV bf16, dQ bf16|fp32
   static constexpr uint32_t oStV = oStK + kTile;
   static constexpr uint32_t oStQ = oStV + kTile;         // dQ staging: bf16 | fp32 [128][DP]
@@ -71,14 +76,14 @@ EVO_DEV void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
   else tmem_ld32(taddr, r);
 }
 
-template <int DP, bool BIAS>
+template <int DP, bool BIAS, bool BIG>
 __global__ void __launch_bounds__(384, 1)
     bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_da,
                      const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
                      const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_b,
                      const BwdFusedArgs a) {
-  using C = FusedCfg<DP, BIAS>;
+  using C = FusedCfg<DP, BIAS, BIG>;
   static_assert(DP == 16 || DP == 32, "fused backward: head dim pad 16 or 32");
   constexpr uint32_t kSw = DP == 32 ? kSw64 : kSw32;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -99,8 +104,12 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[20]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
-  const int Lq_pad = nq * 128, Lk_pad = nk * 128;
+  const int nq_all = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
+  const int Lq_pad = nq_all * 128, Lk_pad = nk * 128;
+  // query tiles t0 .. nq_all-1 (t0 = 2 in the Σ-only pass of a BIG call); nq counts them and
+  // every loop below runs t over [0, nq) with query tile tq = t0 + t
+  const int t0 = a.t0, nq = nq_all - t0;
+  const bool sig_only = a.sigma_only != 0;
   const int c = (int)blockIdx.x % a.nchunks;
   const int grp = (int)blockIdx.x / a.nchunks;
   const int kt = grp % nk, h = grp / nk;
@@ -116,7 +125,9 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(bar_kv + 8 * i, 1);
       mbar_init(bar_in + 8 * i, 1);
       mbar_init(bar_kvfree + 8 * i, 1);
-      mbar_init(bar_infree + 8 * i, 1);
+      // the Σ-only pass frees a Q/dA/vector stage when the 8 compute warps are done with the
+      // tile's lse2/D vectors (the gradient issuer's dQ commit does it otherwise)
+      mbar_init(bar_infree + 8 * i, a.sigma_only ? 8 : 1);
       mbar_init(bar_sp + 8 * i, 1);
       mbar_init(bar_sfree + 8 * i, 4);
       mbar_init(bar_ps + 8 * i, 4);
@@ -132,7 +143,9 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t cb = BIAS ? (uint32_t)Lq_pad : 0u;
+  // Σ_b dSᵀ columns: the query tiles t < sig_n (relative to t0) accumulate in TMEM
+  const int sig_n = BIAS ? (nq < 2 ? nq : 2) : 0;
+  const uint32_t cb = BIAS ? (BIG ? 256u : (uint32_t)Lq_pad) : 0u;
   const uint32_t tDB = tmem, tS0 = tmem + cb, tdV = tS0 + 128, tdK = tdV + DP, tdQ = tdK + DP;
   const uint32_t tP0 = tdQ + DP;  // Pᵀ slot g at +16 g (32 bf16 queries as 16 packed columns)
 
@@ -156,9 +169,9 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
           const uint32_t bar = bar_in + 8 * st;
           mbar_arrive_expect_tx(bar, 2 * C::kTile + 1024);
-          tma_load_4d(qb, &tm_q, bar, 0, t * 128, h, b);
-          tma_load_4d(qb + C::kTile, &tm_da, bar, 0, t * 128, h, b);
-          const int64_t vrow = ((int64_t)b * a.H + h) * Lq_pad + t * 128;
+          tma_load_4d(qb, &tm_q, bar, 0, (t0 + t) * 128, h, b);
+          tma_load_4d(qb + C::kTile, &tm_da, bar, 0, (t0 + t) * 128, h, b);
+          const int64_t vrow = ((int64_t)b * a.H + h) * Lq_pad + (t0 + t) * 128;
           bulk_load(s0 + C::oVec + st * 1024, a.lse2 + vrow, 512, bar);
           bulk_load(s0 + C::oVec + st * 1024 + 512, a.Dvec + vrow, 512, bar);
         }
@@ -197,6 +210,8 @@ __global__ void __launch_bounds__(384, 1)
                     kk > 0);
         umma_commit(bar_sp);
         umma_commit(bar_sp + 8);
+        if (sig_only && sss == 2 && stt == nq - 1)  // no gradient MMAs in the Σ-only pass:
+          umma_commit(bar_kvfree + 8 * kvs);         // the Sᵀ/dPᵀ MMAs are K/V's last readers
         sss += 2;
         if (sss >= 4) {
           sss = 0;
@@ -208,7 +223,7 @@ __global__ void __launch_bounds__(384, 1)
     // ------------------------------------------------------------------ gradient-MMA issuer
     // dV/dK of sub-tile i once its Pᵀ/dSᵀ are in smem; the dQ part after a tile's 4th.  A
     // separate thread from the Sᵀ issuer, so neither stream waits on the other's events.
-    if (lane == 0) {
+    if (lane == 0 && !sig_only) {
       constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, 0, 1);  // dV, dK (B MN-major)
       constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, 1, 1);   // dQ (A, B MN-major)
       int dbi = 0, dtt = 0, dss = 0;  // coordinates of sub-tile i
@@ -223,7 +238,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile + dss * 32 * C::kRowBytes;
         const uint32_t ab = qb + C::kTile;
-        const uint32_t db = s0 + C::oDS + st * 32768 + dss * 8192;
+        const uint32_t db = s0 + C::oDS + (BIG ? 0 : st) * 32768 + dss * 8192;
         const uint32_t acc0 = (dtt > 0 || dss > 0) ? 1u : 0u;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)  // dV += Pᵀ·dA (K = 32 queries; A = Pᵀ from TMEM)
@@ -241,10 +256,10 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tdQ, make_sdesc(s0 + C::oDS + st * 32768 + kk * 1024, 8192, 512, kSw64),
+            umma_bf16(tdQ, make_sdesc(s0 + C::oDS + (BIG ? 0 : st) * 32768 + kk * 1024, 8192, 512, kSw64),
                       make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                       idesc_q, kk > 0 ? 1u : 0u);
-          umma_commit(bar_dq + 8 * st);
+          umma_commit(bar_dq + 8 * (BIG ? 0 : st));
           TL(6, T);  // dQ issued
           // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the groups' hand-offs;
           // dV/dK/dQ: this thread) is done once these commits land
@@ -275,20 +290,35 @@ __global__ void __launch_bounds__(384, 1)
           mbar_arrive_expect_tx(bar_bias, (uint32_t)(Lq_pad / 64) * 16384u);
           for (int sg = 0; sg < Lq_pad / 64; ++sg)
             tma_load_4d(sBias + sg * 16384, &tm_b, bar_bias, sg * 64, k0, h, 0);
-        } else {
+        } else if (!BIG) {
           mbar_arrive_expect_tx(bar_bias, 65536u);
           tma_load_4d(s0 + C::oDS, &tm_b, bar_bias, k0, 0, h, 0);
           tma_load_4d(s0 + C::oDS + 32768, &tm_b, bar_bias, k0 + 64, 0, h, 0);
         }
       }
-      mbar_wait(bar_bias, 0);
-      if (a.bmode != 2) {
+      if (a.bmode == 2 || !BIG) mbar_wait(bar_bias, 0);
+      // k-contiguous: one pass over all queries ([256 q][64 k] x 2 staged), or for BIG passes of
+      // 128 queries ([128 q][64 k] x 2 = the single 32 KB dSᵀ buffer)
+      const int npass = (a.bmode != 2 && BIG) ? Lq_pad / 128 : (a.bmode != 2 ? 1 : 0);
+      for (int ps = 0; ps < npass; ++ps) {
+        const int qb0 = BIG ? ps * 128 : 0;                  // first query of the pass
+        const int nq8 = BIG ? 16 : Lq_pad / 8;              // 8-query blocks in the pass
+        const uint32_t kbox = BIG ? 16384u : 32768u;        // staged [q][64 k] box bytes
+        if (BIG) {
+          if (tid == 0) {
+            mbar_arrive_expect_tx(bar_bias, 32768u);
+            tma_load_4d(s0 + C::oDS, &tm_b, bar_bias, k0, qb0, h, 0);
+            tma_load_4d(s0 + C::oDS + 16384, &tm_b, bar_bias, k0 + 64, qb0, h, 0);
+          }
+          mbar_wait(bar_bias, ps & 1);
+        }
         const int mi = lane >> 3, ri = lane & 7;
-        for (int gi = w; gi < (Lq_pad / 8) * 4; gi += 8) {  // x4 group: q block q8, k blocks 4 kk..4 kk+3
-          const int q8 = gi >> 2, k8 = (gi & 3) * 4 + mi;
-          const uint32_t q = (uint32_t)(q8 * 8 + ri);
-          const uint32_t src = s0 + C::oDS + (uint32_t)(k8 >> 3) * 32768u + q * 128u +
-                               ((((uint32_t)k8 & 7u) ^ (q & 7u)) << 4);
+        for (int gi = w; gi < nq8 * 4; gi += 8) {  // x4 group: q block q8, k blocks 4 kk..4 kk+3
+          const int q8l = gi >> 2, k8 = (gi & 3) * 4 + mi;
+          const int q8 = qb0 / 8 + q8l;
+          const uint32_t ql = (uint32_t)(q8l * 8 + ri);
+          const uint32_t src = s0 + C::oDS + (uint32_t)(k8 >> 3) * kbox + ql * 128u +
+                               ((((uint32_t)k8 & 7u) ^ (ql & 7u)) << 4);
           uint32_t r0, r1, r2, r3;
           asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
                        : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -300,6 +330,7 @@ __global__ void __launch_bounds__(384, 1)
                        "r"(r0), "r"(r1), "r"(r2), "r"(r3)
                        : "memory");
         }
+        if (BIG) named_bar_sync(1, 256);  // the staging is reloaded by the next pass
       }
       named_bar_sync(1, 256);
     }
@@ -352,7 +383,8 @@ __global__ void __launch_bounds__(384, 1)
     // dQ part of tile Tq (group 1), once its dQ MMA has landed: bf16 rows when there is one key
     // tile, else this key tile's fp32 part (dq_convert sums the parts); swizzled staging + TMA store
     auto drain_q = [&](int Tq) {
-      mbar_wait(bar_dq + 8 * (Tq & 1), (Tq >> 1) & 1);
+      if (BIG) mbar_wait(bar_dq, Tq & 1);
+      else mbar_wait(bar_dq + 8 * (Tq & 1), (Tq >> 1) & 1);
       if (qd == 0 && lane == 0) TL(7, Tq);  // dQ landed (drain)
       tc_fence_after();
       if (lane == 0) bulk_wait_group_read0();
@@ -375,10 +407,10 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t rb = nk == 1 ? kRbB : (uint32_t)(DP * 4);
         if (nk > 1 && a.dq_reduce)  // TMA .add at L2 into one fp32 accumulator (bwd_pre zeroed it),
           // evict_last so the lines stay in L2 for the other key tiles' adds and for dq_convert
-          tma_reduce_add_4d_hint(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h, bq,
+          tma_reduce_add_4d_hint(&tm_dq, s0 + C::oStQ + slice * rb, 0, (t0 + Tq % nq) * 128 + (int)slice, h, bq,
                                  l2_policy_evict_last());
         else
-          tma_store_4d(&tm_dq, s0 + C::oStQ + slice * rb, 0, (Tq % nq) * 128 + (int)slice, h,
+          tma_store_4d(&tm_dq, s0 + C::oStQ + slice * rb, 0, (t0 + Tq % nq) * 128 + (int)slice, h,
                        nk == 1 ? bq : kt * a.B + bq);
         bulk_commit_group();
       }
@@ -416,14 +448,16 @@ __global__ void __launch_bounds__(384, 1)
       if (qd == 0 && lane == 0) TL(2, j);  // S landed
       tc_fence_after();
       uint32_t rs[32], rd[32];
-      const int qcol = t * 128 + s * 32;  // first query of this sub-tile
+      const int qcol = (t0 + t) * 128 + s * 32;  // first query of this sub-tile
+      const int scol = t * 128 + s * 32;         // its Σ column (query tiles t < sig_n)
+      const bool do_sig = BIAS && t < sig_n;
       // Σ_b dSᵀ so far for these 32 columns (this thread's own lane and columns, last written
       // one batch row ago): loaded with Sᵀ/dPᵀ so one wait covers all three
       uint32_t acc[32];
       {
         tmem_ld32(tS0 + 32 * g + lane_base, rs);
         tmem_ld32(tS0 + 64 + 32 * g + lane_base, rd);
-        if (BIAS && bi > 0) tmem_ld32(tDB + lane_base + qcol, acc);
+        if (do_sig && bi > 0) tmem_ld32(tDB + lane_base + scol, acc);
       }
       tmem_wait_ld();
       if (qd == 0 && lane == 0) TL(11, j);  // Sᵀ/dPᵀ/Σ in registers
@@ -472,7 +506,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) ds[i] = 0.f;
       }
-      if (BIAS) {  // Σ_b dSᵀ in TMEM (this thread's lane, this sub-tile's 32 query columns)
+      if (do_sig) {  // Σ_b dSᵀ in TMEM (this thread's lane, this sub-tile's 32 query columns)
         if (bi == 0) {  // first batch row of the chunk initialises the (uninitialised) TMEM
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[i] = __float_as_uint(ds[i]);
@@ -486,20 +520,36 @@ __global__ void __launch_bounds__(384, 1)
             acc[i + 1] = __float_as_uint(hi);
           }
         }
-        tmem_st32(tDB + lane_base + qcol, acc);
+        tmem_st32(tDB + lane_base + scol, acc);
+      }
+      if (sig_only) {  // Σ-only pass: no Pᵀ/dSᵀ hand-off, no gradient MMAs, no drains
+        if (s >= 2) {  // this warp's last sub-tile of the tile: its lse2/D stage may be reloaded
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_infree + 8 * st);
+        }
+        s += 2;
+        if (s >= 4) {
+          s -= 4;
+          if (++t == nq) { t = 0; ++bi; }
+        }
+        continue;
       }
       // before overwriting: Pᵀ slot g is read by dV(j-2); this tile's dSᵀ buffer (T & 1) by tile
       // T-2's dQ MMA, long done (checked at the group's first sub-tile of a tile)
       if (qd == 0 && lane == 0) TL(9, j);  // math + Σ store done
       if (j >= 2) mbar_wait(bar_mm + 8 * g, ((j - 2) >> 1) & 1);
-      if (s == g && T >= 2) mbar_wait(bar_dq + 8 * st, ((T - 2) >> 1) & 1);
+      if (BIG) {  // single dSᵀ buffer: tile T-1's dQ MMA must have read it
+        if (s == g && T >= 1) mbar_wait(bar_dq, (T - 1) & 1);
+      } else if (s == g && T >= 2) {
+        mbar_wait(bar_dq + 8 * st, ((T - 2) >> 1) & 1);
+      }
       if (qd == 0 && lane == 0) TL(10, j);  // Pᵀ slot / dSᵀ buffer free
       tc_fence_after();
       // Pᵀ -> TMEM slot g (the A operand of the TS-form dV MMA); dSᵀ (block s) rows to smem:
       // this thread's key row, 32 queries = 4 x 16 B, SW64
       tmem_st16(tP0 + g * 16 + lane_base, pk);
       {
-        const uint32_t db = s0 + C::oDS + st * 32768 + s * 8192;
+        const uint32_t db = s0 + C::oDS + (BIG ? 0 : st) * 32768 + s * 8192;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           st_shared_v4(db + pd_off[e], dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
@@ -527,8 +577,10 @@ __global__ void __launch_bounds__(384, 1)
     }
     // ---- tail: last dQ part (group 1) and last dK/dV (group 0); then both write Σ_b dSᵀ
     const int Tl = (J >> 2) - 1;
-    if (g == 0) {
-      mbar_wait(bar_dq + 8 * (Tl & 1), (Tl >> 1) & 1);
+    if (sig_only) {
+    } else if (g == 0) {
+      if (BIG) mbar_wait(bar_dq, Tl & 1);
+      else mbar_wait(bar_dq + 8 * (Tl & 1), (Tl >> 1) & 1);
       tc_fence_after();
       drain_kv(b0 + nb - 1, false);
     } else {
@@ -536,8 +588,9 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (lane == 0) bulk_wait_group0();
     if (BIAS) {  // partial[c][h][q][k0 + row]: this group's 32-query column blocks
-      float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
-      for (int cbk = g; cbk < Lq_pad / 32; cbk += 2) {
+      float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row +
+                   (int64_t)t0 * 128 * Lk_pad;
+      for (int cbk = g; cbk < sig_n * 4; cbk += 2) {
         uint32_t acc[32];
         tmem_ld32(tDB + lane_base + cbk * 32, acc);
         tmem_wait_ld();
@@ -551,10 +604,10 @@ __global__ void __launch_bounds__(384, 1)
   if (w == 0) tmem_dealloc<512>(tmem);
 }
 
-template <int DP, bool BIAS>
+template <int DP, bool BIAS, bool BIG>
 static cudaError_t launch_bwd_fused_t(const BwdFusedLaunch& L, cudaStream_t st) {
-  auto kern = bwd_fused_kernel<DP, BIAS>;
-  const size_t smem = FusedCfg<DP, BIAS>::kSmem;
+  auto kern = bwd_fused_kernel<DP, BIAS, BIG>;
+  const size_t smem = FusedCfg<DP, BIAS, BIG>::kSmem;
   cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nk = (L.args.Lk + 127) / 128;
@@ -573,10 +626,11 @@ extern "C" int evo_debug_timeline_copy(void* dst, size_t bytes) {
 #endif
 
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {
-#define EVO_FUSED_CASE(dp, bb) \
-  if (DP == dp && (has_bias != 0) == bb) return launch_bwd_fused_t<dp, bb>(L, st);
-  EVO_FUSED_CASE(16, false) EVO_FUSED_CASE(16, true)
-  EVO_FUSED_CASE(32, false) EVO_FUSED_CASE(32, true)
+  const bool big = has_bias && ((L.args.Lq + 127) / 128) * 128 > 256;
+#define EVO_FUSED_CASE(dp, bb, bg) \
+  if (DP == dp && (has_bias != 0) == bb && big == bg) return launch_bwd_fused_t<dp, bb, bg>(L, st);
+  EVO_FUSED_CASE(16, false, false) EVO_FUSED_CASE(16, true, false) EVO_FUSED_CASE(16, true, true)
+  EVO_FUSED_CASE(32, false, false) EVO_FUSED_CASE(32, true, false) EVO_FUSED_CASE(32, true, true)
 #undef EVO_FUSED_CASE
   return cudaErrorInvalidValue;
 }

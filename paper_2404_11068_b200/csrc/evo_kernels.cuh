@@ -143,7 +143,10 @@ struct BwdFusedArgs {
   int dq_reduce;  // 1 (only when nk == 2, so 0 + a + b is order-independent and dq stays bitwise
                   // deterministic): both key tiles reduce-add into ONE fp32 accumulator (zeroed
                   // by bwd_pre); 0: one part per key tile, summed in key-tile order by dq_convert
-  int bmode;  // bias: 1 k-contiguous (tm_b box [256 q][64 k]), 2 q-contiguous (box [128 k][64 q])
+  int bmode;  // bias: 1 k-contiguous (tm_b box [256 q][64 k], [128 q][64 k] when Lq > 256),
+              // 2 q-contiguous (box [128 k][64 q])
+  int t0;          // first query tile (0; 2 in the Σ-only pass of a 256 < Lq <= 384 call)
+  int sigma_only;  // 1: only Σ_b dSᵀ of query tiles t0.. (no gradients)
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
@@ -152,10 +155,10 @@ struct BwdFusedLaunch {
 };
 // eligibility + resources of the fused path for head-dim pad DP and padded Lq
 inline bool bwd_fused_supported(int DP, int Lq_pad, bool bias) {
-  // the Σ_b dSᵀ accumulator needs Lq_pad TMEM columns (and the resident biasᵀ Lq_pad·256 B of
-  // smem), so with a bias Lq <= 256; without one any Lq
-  const int cols = (bias ? Lq_pad : 0) + 128 + 3 * DP + 32;  // Σ | Sᵀ,dPᵀ | dV dK dQ | Pᵀ x2
-  return (!bias || Lq_pad <= 256) && cols <= 512 && (DP == 16 || DP == 32);
+  // the Σ_b dSᵀ accumulator needs up to 256 TMEM columns (queries beyond 256 get a Σ-only
+  // second pass) and the resident biasᵀ Lq_pad·256 B of smem, so with a bias Lq <= 384
+  const int cols = (bias ? (Lq_pad < 256 ? Lq_pad : 256) : 0) + 128 + 3 * DP + 32;
+  return (!bias || Lq_pad <= 384) && cols <= 512 && (DP == 16 || DP == 32);
 }
 inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
   const int groups = H * nk;
