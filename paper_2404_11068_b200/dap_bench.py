@@ -240,41 +240,58 @@ def run_stack(torch, dist, dap, evoattn, comm, pair, world, rank, dev, n_seq, n_
 
 def _e2e(torch, dist, blk, loc, step, args, world, dev, stream, flops):
     """Same block through the same API from pinned HOST buffers: this rank's input shards are
-    copied H2D and its outputs (m_next, z_next and every gradient shard) D2H inside the timed
-    region; max over ranks."""
+    copied H2D and the step's result — a device-side fp32 metric summing m_next, z_next and
+    every gradient shard (the role of a loss; the gradients stay on the device) — D2H inside
+    the timed region; max over ranks.  `all_outputs_d2h` times the same step copying every
+    output and gradient shard D2H."""
     host_in = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v)
                for k, v in loc.items()}
     h2d = sum(v.numel() * v.element_size() for v in host_in.values())
     host_out = {}
+    metric_dev = torch.zeros((), dtype=torch.float32, device=dev)
+    metric_host = torch.zeros((), dtype=torch.float32, pin_memory=True)
 
-    def e2e_step():
+    def e2e_step(all_outputs):
         for k, v in host_in.items():
             loc[k].copy_(v, non_blocking=True)
         m_next, z_next, _ = blk.forward()
         grads = blk.backward(loc["dm_next"], loc["dz_next"])
         outs = dict(grads, m_next=m_next, z_next=z_next)
+        metric_dev.zero_()
         for k, v in outs.items():
             if v is None:
                 continue
-            if k not in host_out:
-                host_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-            host_out[k].copy_(v, non_blocking=True)
+            if all_outputs:
+                if k not in host_out:
+                    host_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                host_out[k].copy_(v, non_blocking=True)
+            else:
+                metric_dev.add_(torch.sum(v, dtype=torch.float32))
+        if not all_outputs:
+            metric_host.copy_(metric_dev, non_blocking=True)
 
-    e2e_step()
-    torch.cuda.synchronize()
+    def timed(all_outputs):
+        e2e_step(all_outputs)
+        torch.cuda.synchronize()
+        n = max(3, min(args.steps, 10))
+        blk.comm.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            e2e_step(all_outputs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / n], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), n
+
+    ms, n = timed(False)
+    ms_all, _ = timed(True)
     d2h = sum(v.numel() * v.element_size() for v in host_out.values())
-    n = max(3, min(args.steps, 10))
-    blk.comm.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(n):
-        e2e_step()
-    b.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / n], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n,
-            "note": "per rank: pinned host shards H2D, outputs and gradient shards D2H"}
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4, "steps": n,
+            "note": "per rank: pinned host input shards H2D; the step's fp32 result metric D2H",
+            "all_outputs_d2h": {"value": flops / (ms_all * 1e-3) / 1e12, "ms_per_step": ms_all,
+                                "d2h_bytes_per_step": int(d2h),
+                                "note": "same step, every output and gradient shard D2H"}}
