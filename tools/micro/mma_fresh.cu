@@ -7,7 +7,7 @@ using namespace evo;
 
 // MODE 0: same A/B every MMA; 1: A and B rotate over 8 tiles (K-major SW64); 2: rotate, B MN-major;
 // 3: TS (A from TMEM), B rotates MN-major; 4: rotate A K-major SW128 128-B rows (the Sᵀ form)
-template <int N, int MODE>
+template <int N, int MODE, int NACC = 2>
 __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) 
       const uint64_t ad = MODE == 4 ? make_sdesc(abase, 16, 1024, kSw128) : make_sdesc(abase, 16, 512, kSw64);
       const uint64_t bd = (MODE == 2 || MODE == 3) ? make_sdesc(bbase, 8192, 512, kSw64)
                                                    : make_sdesc(bbase, 16, 512, kSw64);
-      const uint32_t d = tm + (uint32_t)((i & 1) * N);
+      const uint32_t d = tm + (uint32_t)((i % NACC) * N);
       if (MODE == 3) umma_bf16_ts(d, tm + 256 + (i & 7) * 8, bd, idesc, 1);
       else umma_bf16(d, ad, bd, idesc, 1);
     }
@@ -48,22 +48,30 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) 
   if (threadIdx.x < 32) tmem_dealloc<512>(tm);
 }
 
-template <int N, int MODE>
+template <int N, int MODE, int NACC = 2>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 16);
-  auto f = k<N, MODE>;
+  auto f = k<N, MODE, NACC>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   f<<<148, 128, 200 * 1024>>>(d, 16);
   f<<<148, 128, 200 * 1024>>>(d, 4096);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("N=%3d %-34s %6.1f cyc/MMA [%s]\n", N, name, (double)h / 4096, cudaGetErrorString(e));
+  printf("N=%3d nacc=%d %-34s %6.1f cyc/MMA [%s]\n", N, NACC, name, (double)h / 4096, cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
+  run<32, 1, 1>("SS fresh, ONE accumulator (dependent)");
+  run<32, 1, 2>("SS fresh, 2 accumulators alternating");
+  run<32, 1, 4>("SS fresh, 4 accumulators");
+  run<32, 2, 1>("SS fresh Bmn, ONE accumulator");
+  run<32, 3, 1>("TS fresh, ONE accumulator");
+  run<32, 3, 2>("TS fresh, 2 accumulators");
+  run<64, 1, 1>("SS fresh N64, ONE accumulator");
+  run<32, 0, 1>("SS same tiles, ONE accumulator");
   run<32, 0>("SS same tiles");
   run<32, 1>("SS fresh tiles (K-major)");
   run<32, 2>("SS fresh tiles (B MN-major)");
