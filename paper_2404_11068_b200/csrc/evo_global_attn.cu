@@ -28,7 +28,7 @@ struct GaArgs {
   const float *lse_in, *qbar_in;
 };
 
-constexpr int kGaThreads = 256;
+constexpr int kGaThreads = 512;
 
 EVO_DEV float ga_sigmoid(float x) { return 1.f / (1.f + __expf(-x)); }
 
@@ -71,6 +71,36 @@ EVO_DEV float block_max(float x, float* red) {
   return t;
 }
 
+// block-wide reduction of H <= 16 values per thread at once (max or sum; every thread gets the
+// H results): one shuffle tree per head and a single pair of barriers instead of one per head
+template <bool MAX>
+EVO_DEV void block_reduce_heads(float (&v)[16], int H, float* red) {
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    if (h >= H) break;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float u = __shfl_xor_sync(0xffffffffu, v[h], o);
+      v[h] = MAX ? fmaxf(v[h], u) : v[h] + u;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int h = 0; h < 16; ++h)
+      if (h < H) red[w * 16 + h] = v[h];
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    if (h >= H) break;
+    float t = MAX ? -INFINITY : 0.f;
+    for (int i = 0; i < kGaThreads / 32; ++i) t = MAX ? fmaxf(t, red[i * 16 + h]) : t + red[i * 16 + h];
+    v[h] = t;
+  }
+  __syncthreads();  // red may be reused right after
+}
+
 // Σ over the column's kept sequences of x[b,s,h,:] (slot layout: (s, h, 8-chunk)); result
 // (H·D floats) in out[], divided by `div`
 template <int D>
@@ -83,12 +113,23 @@ EVO_DEV void ga_mean_over_s(const GaArgs& a, int64_t b, const __nv_bfloat16* x, 
   const int h = slot / NC, c = slot % NC;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (grp < ngrp) {
-    for (int s = grp; s < a.S; s += ngrp) {
-      if (!ga_keep(a, b, s)) continue;
-      float r[8];
-      ga_load<8>(x + b * sb + (int64_t)s * ss + (int64_t)h * sh + c * 8, r);
+    for (int s0 = grp; s0 < a.S; s0 += 4 * ngrp) {  // four rows' loads in flight together
+      uint4 u[4];
+      bool ok[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += r[e];
+      for (int j = 0; j < 4; ++j) {
+        const int s = s0 + j * ngrp;
+        ok[j] = s < a.S && ga_keep(a, b, s);
+        u[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(x + b * sb + (int64_t)s * ss +
+                                                            (int64_t)h * sh + c * 8))
+                     : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // rows summed in s order (fixed per thread)
+        const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { acc[2 * e] += bf16_lo(w[e]); acc[2 * e + 1] += bf16_hi(w[e]); }
+      }
     }
   }
   __syncthreads();
@@ -174,21 +215,32 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_fwd_kernel(const GaArg
   if (cnt > 0) {
     ga_scores<D>(a, b, sQ, sA);
     __syncthreads();
-    for (int h = 0; h < a.H; ++h) {  // softmax statistics per head
-      float m = -INFINITY;
-      for (int t = threadIdx.x; t < a.S; t += kGaThreads) m = fmaxf(m, sA[h * a.S + t]);
-      m = block_max(m, red);
-      float sum = 0.f;
-      for (int t = threadIdx.x; t < a.S; t += kGaThreads) {
-        const float e = sA[h * a.S + t] == -INFINITY ? 0.f : __expf(sA[h * a.S + t] - m);
-        sA[h * a.S + t] = e;
-        sum += e;
-      }
-      sum = block_sum(sum, red);
-      if (threadIdx.x == 0) {
-        sN[h] = 1.f / sum;
-        a.lse[b * a.H + h] = m + __logf(sum);
-      }
+    {  // softmax statistics of all heads at once (H <= 16)
+      float m[16], sum[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) { m[h] = -INFINITY; sum[h] = 0.f; }
+      for (int t = threadIdx.x; t < a.S; t += kGaThreads)
+#pragma unroll
+        for (int h = 0; h < 16; ++h)
+          if (h < a.H) m[h] = fmaxf(m[h], sA[h * a.S + t]);
+      block_reduce_heads<true>(m, a.H, red);
+      for (int t = threadIdx.x; t < a.S; t += kGaThreads)
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          if (h >= a.H) break;
+          const float x = sA[h * a.S + t];
+          const float e = x == -INFINITY ? 0.f : __expf(x - m[h]);
+          sA[h * a.S + t] = e;
+          sum[h] += e;
+        }
+      block_reduce_heads<false>(sum, a.H, red);
+      if (threadIdx.x == 0)
+#pragma unroll
+        for (int h = 0; h < 16; ++h)
+          if (h < a.H) {
+            sN[h] = 1.f / sum[h];
+            a.lse[b * a.H + h] = m[h] + __logf(sum[h]);
+          }
     }
     __syncthreads();
     ga_weighted_v<D>(a, b, sA, sN, red, sAt);
@@ -201,17 +253,31 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_fwd_kernel(const GaArg
   // o[b,s,h,:] = σ(g) ⊙ attn[h]
   constexpr int NC = D / 8;
   const int HC = a.H * NC;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)a.S * HC; idx += kGaThreads) {
-    const int s = (int)(idx / HC), slot = (int)(idx % HC), h = slot / NC, c = slot % NC;
-    float gv[8];
-    ga_load<8>(a.g + b * a.g_sb + (int64_t)s * a.g_ss + (int64_t)h * a.g_sh + c * 8, gv);
-    uint32_t w[4];
+  const int64_t nout = (int64_t)a.S * HC;
+  for (int64_t i0 = threadIdx.x; i0 < nout; i0 += 4 * kGaThreads) {  // 4 chunks in flight
+    uint4 gu[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      w[e] = pack_bf16(ga_sigmoid(gv[2 * e]) * sAt[h * D + c * 8 + 2 * e],
-                       ga_sigmoid(gv[2 * e + 1]) * sAt[h * D + c * 8 + 2 * e + 1]);
-    *reinterpret_cast<uint4*>(a.o + b * a.o_sb + (int64_t)s * a.o_ss + (int64_t)h * a.o_sh + c * 8) =
-        make_uint4(w[0], w[1], w[2], w[3]);
+    for (int j = 0; j < 4; ++j) {
+      const int64_t idx = i0 + j * kGaThreads;
+      const int s = (int)(idx / HC), slot = (int)(idx % HC), h = slot / NC, c = slot % NC;
+      gu[j] = idx < nout ? __ldg(reinterpret_cast<const uint4*>(a.g + b * a.g_sb + (int64_t)s * a.g_ss +
+                                                                (int64_t)h * a.g_sh + c * 8))
+                         : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t idx = i0 + j * kGaThreads;
+      if (idx >= nout) break;
+      const int s = (int)(idx / HC), slot = (int)(idx % HC), h = slot / NC, c = slot % NC;
+      const uint32_t gw[4] = {gu[j].x, gu[j].y, gu[j].z, gu[j].w};
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = pack_bf16(ga_sigmoid(bf16_lo(gw[e])) * sAt[h * D + c * 8 + 2 * e],
+                         ga_sigmoid(bf16_hi(gw[e])) * sAt[h * D + c * 8 + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(a.o + b * a.o_sb + (int64_t)s * a.o_ss + (int64_t)h * a.o_sh + c * 8) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
@@ -263,6 +329,7 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_bwd_kernel(const GaArg
     const int h = slot / NC, c = slot % NC;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (grp < ngrp) {
+#pragma unroll 2
       for (int s = grp; s < a.S; s += ngrp) {
         float gv[8], dov[8];
         ga_load<8>(a.g + b * a.g_sb + (int64_t)s * a.g_ss + (int64_t)h * a.g_sh + c * 8, gv);
@@ -294,13 +361,16 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_bwd_kernel(const GaArg
   }
   // per key t: da_h = dattn_h·v_t, dv_t = Σ_h a_ht dattn_h; then Dh = Σ_t a·da
   float dh_part[16];
+#pragma unroll
   for (int h = 0; h < 16; ++h) dh_part[h] = 0.f;
   for (int t = threadIdx.x; t < a.S; t += kGaThreads) {
     float vv[D], dvv[D];
     ga_load<D>(a.v + b * a.v_sb + (int64_t)t * a.v_ss, vv);
 #pragma unroll
     for (int d = 0; d < D; ++d) dvv[d] = 0.f;
-    for (int h = 0; h < a.H; ++h) {
+#pragma unroll
+    for (int h = 0; h < 16; ++h) {  // (unrolled with a guard: dh_part stays in registers)
+      if (h >= a.H) break;
       const float w = sA[h * a.S + t];
       float da = 0.f;
 #pragma unroll
@@ -309,7 +379,7 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_bwd_kernel(const GaArg
         dvv[d] = fmaf(w, sDt[h * D + d], dvv[d]);
       }
       sDA[h * a.S + t] = da;
-      if (h < 16) dh_part[h] = fmaf(w, da, dh_part[h]);
+      dh_part[h] = fmaf(w, da, dh_part[h]);
     }
 #pragma unroll
     for (int c = 0; c < D; c += 8) {
@@ -319,10 +389,11 @@ __global__ void __launch_bounds__(kGaThreads) global_attn_bwd_kernel(const GaArg
       *reinterpret_cast<uint4*>(a.dv + b * a.v_sb + (int64_t)t * a.v_ss + c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
   }
-  for (int h = 0; h < a.H; ++h) {
-    const float Dh = block_sum(dh_part[h], red);
-    if (threadIdx.x == 0) sOne[h] = Dh;  // reuse: Dh per head
-  }
+  block_reduce_heads<false>(dh_part, a.H, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int h = 0; h < 16; ++h)
+      if (h < a.H) sOne[h] = dh_part[h];  // reuse: Dh per head
   __syncthreads();
   // dlogit = a ⊙ (da − Dh);  dk_t = scale·Σ_h dlogit_ht q̄_h
   for (int t = threadIdx.x; t < a.S; t += kGaThreads) {
