@@ -64,7 +64,8 @@ def test_dap_block_world1_matches_oracle():
     for name in SHARD_AXIS:
         a = got[name].double().cpu()
         r = torch.from_numpy(ref[name].copy())
-        err = (a - r).norm() / max(r.norm(), 1e-30)  # normwise relative
+        # normwise max relative error, the parity norm of every other GPU test (R9)
+        err = float((a - r).abs().max() / max(float(r.abs().max()), 1e-30))
         assert err < 2e-2, f"{name}: {err:.3e}"
     comm.close()
 
