@@ -198,3 +198,37 @@ def test_bf16_parity_end_node_many_chunks(B, H, L):
     errs, _, _ = run_case(B, H, L, L, 32, seed=7, bias="shared", bias_t=True, gate=True,
                           mask="prefix", mask_t=True, layout="lbhd")
     _assert(errs, torch.bfloat16, f"end-node B={B} H={H} L={L}")
+
+
+def _random_cases(n, seed):
+    """Seeded random problem shapes over the ABI's whole supported space (every kernel path:
+    one to nine key tiles, 256 < L <= 384 with a bias, D = 8..64, per-batch / shared /
+    transposed / no bias, masks with fully-masked rows, gate on/off, every storage layout)."""
+    r = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        D = int(r.choice([8, 16, 32, 64]))
+        bias = r.choice(["shared", "shared", None, "batch"])
+        L = int(r.integers(1, 420))
+        if bias == "batch":
+            L = min(L, 200)
+        B = int(r.integers(1, 5))
+        H = int(r.integers(1, 5))
+        layout = str(r.choice(["blhd", "lbhd", "bhld"]))
+        bias_t = bool(bias == "shared" and r.random() < 0.4 and L % 8 == 0)
+        mask = str(r.choice(["none", "prefix", "prefix_fm"]))
+        out.append((B, H, L, D, None if bias is None else str(bias), bias_t, bool(r.random() < 0.8),
+                    mask, layout == "lbhd", layout))
+    return out
+
+
+RANDOM_CASES = _random_cases(40, seed=2026)
+
+
+@pytest.mark.parametrize("case", RANDOM_CASES, ids=[str(c) for c in RANDOM_CASES])
+def test_random_shapes_parity(case):
+    """Randomised sweep (seeded, reproducible): every output vs the oracle, bf16 tolerance."""
+    B, H, L, D, bias, bias_t, gate, mask, mask_t, layout = case
+    errs, _, _ = run_case(B, H, L, L, D, seed=L + 7 * D, bias=bias, bias_t=bias_t, gate=gate,
+                          mask=mask, mask_t=mask_t, layout=layout)
+    _assert(errs, torch.bfloat16, str(case))
