@@ -1,6 +1,6 @@
 """Build the native libraries in-tree (sm_100a only; nvcc cross-compiles without a GPU).
 
-libevoattn.so  <- csrc/evo_{api,fwd_occ,bwd,bwd_fused,f32,pair_bias,global_attn,ln_proj}.cu
+libevoattn.so  <- csrc/evo_{api,fwd_occ,bwd,bwd_fused,bwd_nb,f32,pair_bias,global_attn,ln_proj}.cu
                   (C ABI: include/evo_attn.h, evo_pair_bias.h, evo_global_attn.h, evo_ln_proj.h)
 libevodap.so   <- csrc/evo_dap.cu                  (C ABI: include/evo_dap.h; NCCL 2.28)
 """
@@ -20,7 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", INC, "-I", CSRC]
 
-ATTN_SRCS = ["evo_api.cu", "evo_fwd_occ.cu", "evo_bwd.cu", "evo_bwd_fused.cu", "evo_f32.cu", "evo_pair_bias.cu",
+ATTN_SRCS = ["evo_api.cu", "evo_fwd_occ.cu", "evo_bwd.cu", "evo_bwd_fused.cu", "evo_bwd_nb.cu", "evo_f32.cu",
+             "evo_pair_bias.cu",
              "evo_global_attn.cu", "evo_ln_proj.cu"]
 LIB_ATTN = os.path.join(HERE, "libevoattn.so")
 LIB_DAP = os.path.join(HERE, "libevodap.so")

@@ -559,7 +559,11 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.partial = bm ? reinterpret_cast<float*>(ws + W.partial) : nullptr;
     fa.t0 = 0;
     fa.sigma_only = 0;
-    if ((e = traced(st, "bwd_fused", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), bm != 0, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused");
+    if ((e = traced(st, "bwd_fused", [&] {
+           return bm ? evo::launch_bwd_fused_bf16(F, dpad(d->D), 1, st)
+                     : evo::launch_bwd_nb_bf16(F, dpad(d->D), st);  // no bias: per-tile kernel
+         })) != cudaSuccess)
+      return cuda_fail(e, "bwd_fused");
     if (big) {
       ++nl;
       fa.t0 = 2;

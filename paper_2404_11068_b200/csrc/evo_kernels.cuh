@@ -170,6 +170,9 @@ inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
   return (B + ch - 1) / ch;
 }
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st);
+// the no-bias backward (evo_bwd_nb.cu): same launch block and workspace, one 128-query tile per
+// hand-off (N = 128 Sᵀ/dPᵀ MMAs); DP 16 or 32
+cudaError_t launch_bwd_nb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
 
 struct ReduceArgs {  // dbias[h,q,k] (bias strides) = Σ_c partial[c][h][q][k]
   int nparts, H, Lq, Lk;
