@@ -168,10 +168,18 @@ bool use_fused_bwd(const evo_attn_desc_t* d) {
 // zero-fills, and 0 + a + b = 0 + b + a exactly, so the order of the two adds cannot change a
 // bit; with three or more key tiles fp32 addition is not associative, so every key tile stores
 // its own fp32 part and dq_convert sums the parts in key-tile order 0, 1, ..., nk-1.
+// No bias, several key tiles, enough (b, h) rows to fill the SMs: the no-bias kernel walks all
+// key tiles of a row inside one CTA and accumulates dQ in TMEM in key-tile order (deterministic,
+// no fp32 parts, no dq_convert)
+bool use_nb_kloop(const evo_attn_desc_t* d) {
+  const int nq = (int)((d->Lq + 127) / 128), nk = (int)((d->Lk + 127) / 128);
+  return use_fused_bwd(d) && d->bias_kind == EVO_BIAS_NONE && nk > 1 &&
+         evo::bwd_nb_kloop_fits(dpad(d->D), nq) && d->B * d->H >= num_sms();
+}
 bool use_dq_reduce(const evo_attn_desc_t* d) {
   const int64_t nk = (d->Lk + 127) / 128;
   const int64_t pre_vec = d->B * d->H * ((d->Lq + 127) / 128 * 128) * (d->D / 8);
-  return use_fused_bwd(d) && nk == 2 && d->D % 8 == 0 &&
+  return use_fused_bwd(d) && !use_nb_kloop(d) && nk == 2 && d->D % 8 == 0 &&
          pre_vec < ((int64_t)1 << 31);  // the conditions of bwd_pre's vectorised path
 }
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -185,7 +193,7 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
   w.lse2 = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   w.dvec = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   if (d->has_gate) { w.da = off; off = al256(off + (size_t)rows * d->Lq * d->D * esize(d)); }
-  if (d->dtype == EVO_BF16 && nk > 1) {
+  if (d->dtype == EVO_BF16 && nk > 1 && !use_nb_kloop(d)) {
     // one fp32 accumulator (nk == 2, reduce-add) or one fp32 part per key tile (use_dq_reduce)
     w.dqacc = off;
     const int64_t parts = use_dq_reduce(d) ? 1 : nk;
@@ -514,7 +522,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   const int bm = bias_mode(d);
   if (bm && !make_bias_map(&tb, d, bias)) return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
 
-  float* dqacc = nk > 1 ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
+  const bool kloop = use_nb_kloop(d);
+  float* dqacc = nk > 1 && !kloop ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
   if (W.fused) {
     evo::BwdFusedLaunch F;
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
@@ -527,7 +536,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     // 32-row boxes: each compute warp stores its own TMEM lane quarter
     if (!make_x_map(&F.tm_dk, dk, dt, 2, d->B, d->H, d->Lk, d->D, d->k_str, 32) ||
         !make_x_map(&F.tm_dv, dv, dt, 2, d->B, d->H, d->Lk, d->D, d->v_str, 32) ||
-        !(nk == 1 ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str, 32)
+        !(!dqacc ? make_x_map(&F.tm_dq, dq, dt, 2, d->B, d->H, d->Lq, d->D, d->q_str, 32)
                   : make_x_map(&F.tm_dq, dqacc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                (int64_t)nk * d->B, d->H, d->Lq, d->D, part_str, 32,
                                std::min(dpad(d->D), 32))))
@@ -537,7 +546,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.B = (int)d->B; fa.H = d->H; fa.Lq = d->Lq; fa.Lk = d->Lk; fa.D = d->D;
     fa.scale = d->scale; fa.scale_log2 = d->scale * evo::kLog2e;
     // same chunking as the workspace's dbias partials (ws_layout)
-    fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, nk, num_sms(), &fa.chunk);
+    fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, kloop ? 1 : nk, num_sms(), &fa.chunk);
+    fa.kloop = kloop ? 1 : 0;
     fa.bias = (const __nv_bfloat16*)bias;
     fa.b_sh = d->bias_str[1]; fa.b_sq = d->bias_str[2]; fa.b_sk = d->bias_str[3];
     fa.mask = mask; fa.mask_s0 = d->mask_str[0]; fa.mask_s1 = d->mask_str[1];

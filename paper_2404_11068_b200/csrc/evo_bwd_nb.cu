@@ -77,19 +77,25 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t bar_dqfree = smem_u32(&bars[4 * S + 6]); // the drain warps pulled a tile's dQ
   const uint32_t bar_kvdone = smem_u32(&bars[4 * S + 7]); // a batch row's last dV/dK MMA landed
   const uint32_t bar_dkvfree = smem_u32(&bars[4 * S + 8]);  // the drain warps pulled dK/dV
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[4 * S + 9]);
+  const uint32_t bar_dqrow = smem_u32(&bars[4 * S + 9]);    // kloop: a batch row's dQ is final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[4 * S + 10]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
   const int Lq_pad = nq * 128;
   const int c = (int)blockIdx.x % a.nchunks;
   const int grp = (int)blockIdx.x / a.nchunks;
-  const int kt = grp % nk, h = grp / nk;
-  const int k0 = kt * 128;
+  // a "group" is one (batch row, key tile) pair: its K/V stay resident while its nq query tiles
+  // stream by.  kloop: the CTA walks key tiles 0..nk-1 of each of its batch rows (dQ accumulates
+  // over them in TMEM); otherwise the CTA owns the single key tile ktf
+  const bool kloop = a.kloop != 0;
+  const int nkl = kloop ? nk : 1;
+  const int ktf = kloop ? 0 : grp % nk, h = kloop ? grp : grp / nk;
   const int b0 = c * a.chunk;
   const int nb = min(a.B - b0, a.chunk);
   if (nb <= 0) return;
-  const int NT = nb * nq;  // tiles
+  const int NG = nb * nkl;  // groups
+  const int NT = NG * nq;   // tiles
 
   if (w == 0) tmem_alloc<512>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -108,6 +114,7 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(bar_dqfree, 4);
     mbar_init(bar_kvdone, 1);
     mbar_init(bar_dkvfree, 4);
+    mbar_init(bar_dqrow, 1);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -126,15 +133,16 @@ __global__ void __launch_bounds__(512, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_da);
-      for (int bi = 0; bi < nb; ++bi) {
-        const int b = b0 + bi, kvs = bi % S;
-        if (bi >= S) mbar_wait(bar_kvfree + 8 * kvs, ((bi - S) / S) & 1);
+      for (int gi = 0; gi < NG; ++gi) {
+        const int bi = gi / nkl, kt = kloop ? gi - bi * nkl : ktf;
+        const int b = b0 + bi, kvs = gi % S;
+        if (gi >= S) mbar_wait(bar_kvfree + 8 * kvs, ((gi - S) / S) & 1);
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
         mbar_arrive_expect_tx(bar_kv + 8 * kvs, 2 * C::kTile);
-        tma_load_4d(kb, &tm_k, bar_kv + 8 * kvs, 0, k0, h, b);
-        tma_load_4d(kb + C::kTile, &tm_v, bar_kv + 8 * kvs, 0, k0, h, b);
+        tma_load_4d(kb, &tm_k, bar_kv + 8 * kvs, 0, kt * 128, h, b);
+        tma_load_4d(kb + C::kTile, &tm_v, bar_kv + 8 * kvs, 0, kt * 128, h, b);
         for (int t = 0; t < nq; ++t) {
-          const int T = bi * nq + t, st = T % S;
+          const int T = gi * nq + t, st = T % S;
           if (T >= S) mbar_wait(bar_infree + 8 * st, ((T - S) / S) & 1);
           const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
           const uint32_t bar = bar_in + 8 * st;
@@ -152,10 +160,10 @@ __global__ void __launch_bounds__(512, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);
       for (int T = 0; T < NT; ++T) {
-        const int bi = T / nq, t = T - bi * nq, st = T % S, kvs = bi % S;
+        const int gi = T / nq, t = T - gi * nq, st = T % S, kvs = gi % S;
         if (T >= 1) mbar_wait(bar_sfree, (T - 1) & 1);  // the previous tile's Sᵀ/dPᵀ pulled
         mbar_wait(bar_in + 8 * st, (T / S) & 1);
-        if (t == 0) mbar_wait(bar_kv + 8 * kvs, (bi / S) & 1);
+        if (t == 0) mbar_wait(bar_kv + 8 * kvs, (gi / S) & 1);
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
@@ -176,10 +184,11 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, 0, 1);  // dV, dK (B MN-major)
       constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, 1, 1);   // dQ (A, B MN-major)
       for (int T = 0; T < NT; ++T) {
-        const int bi = T / nq, t = T - bi * nq, st = T % S, kvs = bi % S, ds = T & 1;
+        const int gi = T / nq, t = T - gi * nq, st = T % S, kvs = gi % S, ds = T & 1;
+        const int bi = gi / nkl, kt = kloop ? gi - bi * nkl : ktf;
         mbar_wait(bar_ps, T & 1);
-        // a new batch row overwrites dK/dV: the drain warps must have pulled the previous ones
-        if (t == 0 && bi > 0) mbar_wait(bar_dkvfree, (bi - 1) & 1);
+        // a new group overwrites dK/dV: the drain warps must have pulled the previous ones
+        if (t == 0 && gi > 0) mbar_wait(bar_dkvfree, (gi - 1) & 1);
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
         const uint32_t ab = qb + C::kTile;
@@ -195,18 +204,26 @@ __global__ void __launch_bounds__(512, 1)
                     make_sdesc(qb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                     idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
         umma_commit(bar_mm);
-        if (t == nq - 1) umma_commit(bar_kvdone);  // the row's dK/dV are final
-        // dQ part = dS·K (A = the tile's dSᵀ blocks read MN-major); the drain warps must have
-        // pulled the previous tile's dQ out of TMEM
-        if (T >= 1) mbar_wait(bar_dqfree, (T - 1) & 1);
+        if (t == nq - 1) umma_commit(bar_kvdone);  // the group's dK/dV are final
+        // dQ = dS·K (A = the tile's dSᵀ blocks read MN-major).  kloop: accumulated over the key
+        // tiles in the tile's own TMEM columns, which the drain warps must have pulled for the
+        // previous batch row; otherwise one TMEM dQ the drain pulls after every tile
+        if (kloop) {
+          if (kt == 0 && t == 0 && bi > 0) mbar_wait(bar_dqfree, (bi - 1) & 1);
+        } else if (T >= 1) {
+          mbar_wait(bar_dqfree, (T - 1) & 1);
+        }
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
+        const uint32_t tq = kloop ? tdQ + t * DP : tdQ;
+        const uint32_t acc0 = kloop && kt > 0 ? 1u : 0u;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16(tdQ, make_sdesc(db + kk * 1024, 8192, 512, kSw64),
+          umma_bf16(tq, make_sdesc(db + kk * 1024, 8192, 512, kSw64),
                     make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
-                    idesc_q, kk > 0 ? 1u : 0u);
+                    idesc_q, kk > 0 ? 1u : acc0);
         umma_commit(bar_dq + 8 * ds);
+        if (kloop && kt == nk - 1 && t == nq - 1) umma_commit(bar_dqrow);  // the row's dQ final
         // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the hand-off; dV/dK/dQ:
         // this thread) and, after a row's last tile, of the K/V stage is done once these land
         umma_commit(bar_infree + 8 * st);
@@ -235,9 +252,10 @@ __global__ void __launch_bounds__(512, 1)
       }
     };
     for (int T = 0; T < NT; ++T) {
-      const int bi = T / nq, t = T - bi * nq;
-      if (t == nq - 1) {  // the batch row's dK/dV, once its last dV/dK MMA landed
-        mbar_wait(bar_kvdone, bi & 1);
+      const int gi = T / nq, t = T - gi * nq;
+      const int bi = gi / nkl, kt = kloop ? gi - bi * nkl : ktf;
+      if (t == nq - 1) {  // the group's dK/dV, once its last dV/dK MMA landed
+        mbar_wait(bar_kvdone, gi & 1);
         tc_fence_after();
         if (lane == 0) bulk_wait_group_read0();  // this warp's previous stores left its slices
         __syncwarp();
@@ -249,10 +267,36 @@ __global__ void __launch_bounds__(512, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_4d(&tm_dk, s0 + C::oStK + slice * kRbB, 0, k0 + (int)slice, h, b0 + bi);
-          tma_store_4d(&tm_dv, s0 + C::oStV + slice * kRbB, 0, k0 + (int)slice, h, b0 + bi);
+          tma_store_4d(&tm_dk, s0 + C::oStK + slice * kRbB, 0, kt * 128 + (int)slice, h, b0 + bi);
+          tma_store_4d(&tm_dv, s0 + C::oStV + slice * kRbB, 0, kt * 128 + (int)slice, h, b0 + bi);
           bulk_commit_group();
         }
+      }
+      if (kloop) {
+        // the batch row's dQ of every query tile, once its last key tile's dQ MMA landed:
+        // bf16 through two alternating staging halves
+        if (kt == nk - 1 && t == nq - 1) {
+          mbar_wait(bar_dqrow, bi & 1);
+          tc_fence_after();
+          for (int tq = 0; tq < nq; ++tq) {
+            const uint32_t sb = s0 + C::oStQ + (tq & 1) * (128 * kRbB);
+            if (lane == 0) bulk_wait_group_read<1>();  // the store from this half has left
+            __syncwarp();
+            stage_bf16(sb, tdQ + tq * DP + lane_base, a.scale);
+            if (tq == nq - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_dqfree);  // the next row's dQ MMAs may overwrite
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tm_dq, sb + slice * kRbB, 0, tq * 128 + (int)slice, h, b0 + bi);
+              bulk_commit_group();
+            }
+          }
+        }
+        continue;
       }
       // dQ part of tile T: bf16 rows with one key tile, else this key tile's fp32 part
       // (reduce-add into the one accumulator at nk == 2, its own part otherwise)
@@ -298,30 +342,24 @@ __global__ void __launch_bounds__(512, 1)
     const int row = qd * 32 + lane;      // key row within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
     const uint64_t sl2 = f2_pack(a.scale_log2, a.scale_log2);
-    const int kglob = k0 + row;
-    // hard-mask bits of this thread's key for 32 batch rows from b (all 32 loads in flight)
-    auto load_keep_word = [&](int b) -> uint32_t {
-      if (kglob >= a.Lk) return 0u;
-      if (!a.mask) return ~0u;
-      uint32_t v[32];
-#pragma unroll
-      for (int x = 0; x < 32; ++x)
-        v[x] = b + x < b0 + nb ? (uint32_t)__ldg(a.mask + (int64_t)(b + x) * a.mask_s0 + (int64_t)kglob * a.mask_s1) : 0u;
-      uint32_t wd = 0u;
-#pragma unroll
-      for (int x = 0; x < 32; ++x) wd |= (v[x] != 0u ? 1u : 0u) << x;
-      return wd;
+    // hard-mask byte of this thread's key in group gi (raw: loaded a group ahead, tested late)
+    auto load_keep = [&](int gi) -> uint32_t {
+      if (gi >= NG) return 0u;
+      const int bi = gi / nkl, kg = (kloop ? gi - bi * nkl : ktf) * 128 + row;
+      if (kg >= a.Lk) return 0u;
+      if (!a.mask) return 1u;
+      return (uint32_t)__ldg(a.mask + (int64_t)(b0 + bi) * a.mask_s0 + (int64_t)kg * a.mask_s1);
     };
     uint32_t pd_off[4];  // this thread's row of a [128][32] bf16 SW64 dSᵀ block: 4 chunk offsets
 #pragma unroll
     for (int e = 0; e < 4; ++e) pd_off[e] = swz_offset(row, e, 64);
-    uint32_t keep_word = 0u;
+    uint32_t keep_nx = load_keep(0);
     bool keep = false;
     for (int T = 0; T < NT; ++T) {
-      const int bi = T / nq, t = T - bi * nq, st = T % S, ds = T & 1;
+      const int gi = T / nq, t = T - gi * nq, st = T % S, ds = T & 1;
       if (t == 0) {
-        if ((bi & 31) == 0) keep_word = load_keep_word(b0 + bi);
-        keep = (keep_word >> (bi & 31)) & 1u;
+        keep = keep_nx != 0u;
+        keep_nx = load_keep(gi + 1);
       }
       mbar_wait(bar_sp, T & 1);
       tc_fence_after();
@@ -403,7 +441,7 @@ static cudaError_t launch_bwd_nb_t(const BwdFusedLaunch& L, cudaStream_t st) {
   cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nk = (L.args.Lk + 127) / 128;
-  const long long grid = (long long)L.args.H * nk * L.args.nchunks;
+  const long long grid = (long long)L.args.H * (L.args.kloop ? 1 : nk) * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
   kern<<<(unsigned)grid, 512, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
                                           L.tm_dv, L.args);

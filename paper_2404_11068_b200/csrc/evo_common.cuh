@@ -136,6 +136,8 @@ EVO_DEV float4 ldg_f4_hint(const float* p, uint64_t pol) {
 EVO_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the issuing thread's bulk groups have finished READING shared memory
 EVO_DEV void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+template <int N>
+EVO_DEV void bulk_wait_group_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 EVO_DEV void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 1-D bulk copy global -> shared (16-byte aligned, size multiple of 16)
 EVO_DEV void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes, uint32_t bar) {

@@ -147,6 +147,9 @@ struct BwdFusedArgs {
               // 2 q-contiguous (box [128 k][64 q])
   int t0;          // first query tile (0; 2 in the Σ-only pass of a 256 < Lq <= 384 call)
   int sigma_only;  // 1: only Σ_b dSᵀ of query tiles t0.. (no gradients)
+  int kloop;       // no-bias kernel: 1 = each CTA walks every key tile of its (b, h) rows and
+                   // accumulates dQ of all query tiles in TMEM (bf16 dQ, no fp32 parts);
+                   // 0 = one key tile per CTA (grid H x nk x chunks)
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;
@@ -173,6 +176,9 @@ cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias,
 // the no-bias backward (evo_bwd_nb.cu): same launch block and workspace, one 128-query tile per
 // hand-off (N = 128 Sᵀ/dPᵀ MMAs); DP 16 or 32
 cudaError_t launch_bwd_nb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
+// the key-tile loop of the no-bias kernel keeps nq dQ accumulators (DP columns each) in TMEM
+// next to Sᵀ, dPᵀ, Pᵀ (320 columns), dV and dK
+inline bool bwd_nb_kloop_fits(int DP, int nq) { return 320 + 2 * DP + nq * DP <= 512; }
 
 struct ReduceArgs {  // dbias[h,q,k] (bias strides) = Σ_c partial[c][h][q][k]
   int nparts, H, Lq, Lk;

@@ -119,6 +119,7 @@ DET_CASES = [
     (2, 2, 300, 64, "shared", "blhd"),
     (2, 2, 130, 32, "batch", "blhd"),
     (40, 2, 256, 32, "shared", "blhd"),
+    (40, 4, 384, 32, None, "lbhd"),
 ]
 
 
@@ -188,6 +189,17 @@ def test_bf16_parity_many_batch_rows(B, H, L, bias):
     errs, _, _ = run_case(B, H, L, L, 32, seed=3, bias=bias, gate=True, mask="prefix",
                           mask_t=False, layout="blhd")
     _assert(errs, torch.bfloat16, f"B={B} H={H} L={L} bias={bias}")
+
+
+@pytest.mark.parametrize("B,H,L,D,mask", [(40, 4, 300, 32, "prefix"), (38, 4, 520, 8, "prefix_fm"),
+                                          (150, 1, 256, 16, "prefix"), (37, 4, 512, 32, "prefix_fm")])
+def test_bf16_parity_nobias_key_tile_loop(B, H, L, D, mask):
+    """No bias, several key tiles, B·H >= the SM count: the no-bias backward walks every key
+    tile of a (b, h) row inside one CTA and accumulates dQ of all query tiles in TMEM (no fp32
+    parts); the per-group keep mask, the row-level dQ drain and the ragged last tiles."""
+    errs, _, _ = run_case(B, H, L, L, D, seed=13, bias=None, gate=True, mask=mask,
+                          mask_t=True, layout="lbhd")
+    _assert(errs, torch.bfloat16, f"kloop B={B} H={H} L={L} D={D}")
 
 
 @pytest.mark.parametrize("B,H,L", [(40, 2, 256), (200, 1, 128)])
