@@ -176,6 +176,9 @@ cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias,
 // the no-bias backward (evo_bwd_nb.cu): same launch block and workspace, one 128-query tile per
 // hand-off (N = 128 Sᵀ/dPᵀ MMAs); DP 16 or 32
 cudaError_t launch_bwd_nb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
+// the pair-bias kernel (evo_bwd_pb.cu) for a shared bias with Lq <= 256: 64-query hand-offs
+// processed by all eight compute warps, Σ_b dSᵀ in TMEM; DP 16 or 32
+cudaError_t launch_bwd_pb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
 // the key-tile loop of the no-bias kernel keeps nq dQ accumulators (DP columns each) in TMEM
 // next to Sᵀ, dPᵀ, Pᵀ (320 columns), dV and dK
 inline bool bwd_nb_kloop_fits(int DP, int nq) { return 320 + 2 * DP + nq * DP <= 512; }

@@ -1,5 +1,5 @@
 """Per-kernel device time of one fwd + bwd call (C-ABI trace events) at a given shape.
-python tools/kernel_split.py B H L D bias(0/1/t) [layout bl|lb]"""
+python tools/kernel_split.py B H L D bias(0/1/t) [layout bl|lb] [--lib other.so]"""
 import ctypes
 import os
 import sys
@@ -8,6 +8,11 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import torch  # noqa: E402
 
 from paper_2404_11068_b200 import evoattn  # noqa: E402
+
+if "--lib" in sys.argv:  # A/B against another build of the library (e.g. a previous commit's)
+    i = sys.argv.index("--lib")
+    evoattn._LIB_PATH = os.path.abspath(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 
 Bn, H, L, D = (int(x) for x in sys.argv[1:5])
 bias = sys.argv[5]
