@@ -1,5 +1,7 @@
 // evo_bwd_fused.cu — single-pass bf16 backward on sm_100a: dK, dV, dQ and the pair-bias
 // gradient of one (head, 128-key tile) for a chunk of batch rows, in one persistent CTA.
+// Shipped for a shared bias with 256 < Lq <= 384 only (the BIG instantiation, BASELINE cfg 5):
+// Lq <= 256 with a bias runs on evo_bwd_pb.cu and no bias on evo_bwd_nb.cu.
 //
 // Same arithmetic as evo_bwd.cu's bwd_main + bwd_bias (SPEC.md L168
 // recompute backward; dbias = Σ_b dS over the broadcast axis, PAPER.md L294 / north star), but
@@ -625,13 +627,13 @@ extern "C" int evo_debug_timeline_copy(void* dst, size_t bytes) {
 }
 #endif
 
+// Only the BIG instantiation ships: Lq <= 256 with a bias runs on evo_bwd_pb.cu, no bias on
+// evo_bwd_nb.cu (both faster)
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {
   const bool big = has_bias && ((L.args.Lq + 127) / 128) * 128 > 256;
-#define EVO_FUSED_CASE(dp, bb, bg) \
-  if (DP == dp && (has_bias != 0) == bb && big == bg) return launch_bwd_fused_t<dp, bb, bg>(L, st);
-  EVO_FUSED_CASE(16, false, false) EVO_FUSED_CASE(16, true, false) EVO_FUSED_CASE(16, true, true)
-  EVO_FUSED_CASE(32, false, false) EVO_FUSED_CASE(32, true, false) EVO_FUSED_CASE(32, true, true)
-#undef EVO_FUSED_CASE
+  if (!big) return cudaErrorInvalidValue;
+  if (DP == 16) return launch_bwd_fused_t<16, true, true>(L, st);
+  if (DP == 32) return launch_bwd_fused_t<32, true, true>(L, st);
   return cudaErrorInvalidValue;
 }
 
