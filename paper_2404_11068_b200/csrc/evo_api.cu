@@ -176,10 +176,19 @@ bool use_nb_kloop(const evo_attn_desc_t* d) {
   return use_fused_bwd(d) && d->bias_kind == EVO_BIAS_NONE && nk > 1 &&
          evo::bwd_nb_kloop_fits(dpad(d->D), nq) && d->B * d->H >= num_sms();
 }
+// Shared bias, Lq <= 256, exactly two key tiles (the bias modules at N_res / N_seq = 256): the
+// pair-bias kernel runs the two key tiles of a (h, chunk) as a 2-CTA cluster and sums dQ on
+// chip (dQ_0 + dQ_1 in that order: deterministic, no fp32 accumulator, no dq_convert)
+bool use_dq_pair(const evo_attn_desc_t* d) {
+  const int nk = (int)((d->Lk + 127) / 128), Lq_pad = (int)((d->Lq + 127) / 128) * 128;
+  // rank 0/1 store their dq rows with 16-B vector stores: D % 8 == 0 and 16-B aligned rows
+  const bool vec = d->D % 8 == 0 && d->q_str[0] % 8 == 0 && d->q_str[1] % 8 == 0 && d->q_str[2] % 8 == 0;
+  return use_fused_bwd(d) && d->bias_kind == EVO_BIAS_SHARED && Lq_pad <= 256 && nk == 2 && vec;
+}
 bool use_dq_reduce(const evo_attn_desc_t* d) {
   const int64_t nk = (d->Lk + 127) / 128;
   const int64_t pre_vec = d->B * d->H * ((d->Lq + 127) / 128 * 128) * (d->D / 8);
-  return use_fused_bwd(d) && !use_nb_kloop(d) && nk == 2 && d->D % 8 == 0 &&
+  return use_fused_bwd(d) && !use_nb_kloop(d) && !use_dq_pair(d) && nk == 2 && d->D % 8 == 0 &&
          pre_vec < ((int64_t)1 << 31);  // the conditions of bwd_pre's vectorised path
 }
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -193,7 +202,7 @@ WsLayout ws_layout(const evo_attn_desc_t* d) {
   w.lse2 = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   w.dvec = off; off = al256(off + (size_t)rows * Lq_pad * 4);
   if (d->has_gate) { w.da = off; off = al256(off + (size_t)rows * d->Lq * d->D * esize(d)); }
-  if (d->dtype == EVO_BF16 && nk > 1 && !use_nb_kloop(d)) {
+  if (d->dtype == EVO_BF16 && nk > 1 && !use_nb_kloop(d) && !use_dq_pair(d)) {
     // one fp32 accumulator (nk == 2, reduce-add) or one fp32 part per key tile (use_dq_reduce)
     w.dqacc = off;
     const int64_t parts = use_dq_reduce(d) ? 1 : nk;
@@ -522,8 +531,8 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
   const int bm = bias_mode(d);
   if (bm && !make_bias_map(&tb, d, bias)) return fail(EVO_E_CUDA, "cuTensorMapEncodeTiled failed for bias");
 
-  const bool kloop = use_nb_kloop(d);
-  float* dqacc = nk > 1 && !kloop ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
+  const bool kloop = use_nb_kloop(d), dq_pair = use_dq_pair(d);
+  float* dqacc = nk > 1 && !kloop && !dq_pair ? reinterpret_cast<float*>(ws + W.dqacc) : nullptr;
   if (W.fused) {
     evo::BwdFusedLaunch F;
     F.tm_q = tq; F.tm_k = tk; F.tm_v = tv; F.tm_da = tda;
@@ -548,6 +557,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     // same chunking as the workspace's dbias partials (ws_layout)
     fa.nchunks = evo::bwd_fused_nchunks((int)d->B, d->H, kloop ? 1 : nk, num_sms(), &fa.chunk);
     fa.kloop = kloop ? 1 : 0;
+    fa.dq_pair = dq_pair ? 1 : 0;
     fa.bias = (const __nv_bfloat16*)bias;
     fa.b_sh = d->bias_str[1]; fa.b_sq = d->bias_str[2]; fa.b_sk = d->bias_str[3];
     fa.mask = mask; fa.mask_s0 = d->mask_str[0]; fa.mask_s1 = d->mask_str[1];

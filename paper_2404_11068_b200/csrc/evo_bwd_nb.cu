@@ -27,6 +27,18 @@
 
 namespace evo {
 
+#ifdef EVO_TIMELINE
+// Debug builds only (tools/nb_timeline.py compiles a separate library with -DEVO_TIMELINE):
+// clock64 stamps of CTAs 0 and 1, 14 event kinds x 512 tiles each.
+__device__ unsigned long long g_tlnb[2][14][512];
+#define NTL(ev, i)                                                               \
+  do {                                                                           \
+    if (blockIdx.x < 2 && (i) < 512) g_tlnb[blockIdx.x][ev][i] = clock64();      \
+  } while (0)
+#else
+#define NTL(ev, i) do { } while (0)
+#endif
+
 template <int DP>
 struct NbCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
@@ -144,6 +156,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int t = 0; t < nq; ++t) {
           const int T = gi * nq + t, st = T % S;
           if (T >= S) mbar_wait(bar_infree + 8 * st, ((T - S) / S) & 1);
+          NTL(11, T);  // Q/dA load issued
           const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
           const uint32_t bar = bar_in + 8 * st;
           mbar_arrive_expect_tx(bar, 2 * C::kTile + 1024);
@@ -164,6 +177,7 @@ __global__ void __launch_bounds__(512, 1)
         if (T >= 1) mbar_wait(bar_sfree, (T - 1) & 1);  // the previous tile's Sᵀ/dPᵀ pulled
         mbar_wait(bar_in + 8 * st, (T / S) & 1);
         if (t == 0) mbar_wait(bar_kv + 8 * kvs, (gi / S) & 1);
+        NTL(12, T);  // S issuer ready
         tc_fence_after();
         const uint32_t kb = s0 + C::oKV + kvs * 2 * C::kTile;
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
@@ -176,6 +190,7 @@ __global__ void __launch_bounds__(512, 1)
           umma_bf16(tdP, make_sdesc(kb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw),
                     make_sdesc(qb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s, kk > 0);
         umma_commit(bar_sp);
+        NTL(0, T);  // Sᵀ/dPᵀ issued
       }
     }
   } else if (w == 10) {
@@ -187,8 +202,10 @@ __global__ void __launch_bounds__(512, 1)
         const int gi = T / nq, t = T - gi * nq, st = T % S, kvs = gi % S, ds = T & 1;
         const int bi = gi / nkl, kt = kloop ? gi - bi * nkl : ktf;
         mbar_wait(bar_ps, T & 1);
+        NTL(6, T);  // hand-off seen
         // a new group overwrites dK/dV: the drain warps must have pulled the previous ones
         if (t == 0 && gi > 0) mbar_wait(bar_dkvfree, (gi - 1) & 1);
+        NTL(7, T);  // dK/dV free
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
         const uint32_t ab = qb + C::kTile;
@@ -204,6 +221,7 @@ __global__ void __launch_bounds__(512, 1)
                     make_sdesc(qb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                     idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
         umma_commit(bar_mm);
+        NTL(8, T);  // dV/dK issued
         if (t == nq - 1) umma_commit(bar_kvdone);  // the group's dK/dV are final
         // dQ = dS·K (A = the tile's dSᵀ blocks read MN-major).  kloop: accumulated over the key
         // tiles in the tile's own TMEM columns, which the drain warps must have pulled for the
@@ -223,6 +241,7 @@ __global__ void __launch_bounds__(512, 1)
                     make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                     idesc_q, kk > 0 ? 1u : acc0);
         umma_commit(bar_dq + 8 * ds);
+        NTL(9, T);  // dQ issued
         if (kloop && kt == nk - 1 && t == nq - 1) umma_commit(bar_dqrow);  // the row's dQ final
         // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the hand-off; dV/dK/dQ:
         // this thread) and, after a row's last tile, of the K/V stage is done once these land
@@ -256,6 +275,7 @@ __global__ void __launch_bounds__(512, 1)
       const int bi = gi / nkl, kt = kloop ? gi - bi * nkl : ktf;
       if (t == nq - 1) {  // the group's dK/dV, once its last dV/dK MMA landed
         mbar_wait(bar_kvdone, gi & 1);
+        if (qd == 0 && lane == 0) NTL(10, T);  // dK/dV landed (drain)
         tc_fence_after();
         if (lane == 0) bulk_wait_group_read0();  // this warp's previous stores left its slices
         __syncwarp();
@@ -361,8 +381,10 @@ __global__ void __launch_bounds__(512, 1)
         keep = keep_nx != 0u;
         keep_nx = load_keep(gi + 1);
       }
+      if (w == 0 && lane == 0) NTL(1, T);  // waits for Sᵀ/dPᵀ
       mbar_wait(bar_sp, T & 1);
       tc_fence_after();
+      if (w == 0 && lane == 0) NTL(2, T);  // Sᵀ/dPᵀ landed
       mbar_wait(bar_in + 8 * st, (T / S) & 1);  // lse2 / D of this query tile visible
 #pragma unroll 1
       for (int hb = 0; hb < 2; ++hb) {  // two 32-query batches of this warp's 64 queries
@@ -407,11 +429,13 @@ __global__ void __launch_bounds__(512, 1)
           for (int i = 0; i < 16; ++i) { pk[i] = 0u; dk2[i] = 0u; }
         }
         if (hb == 0) {
+          if (w == 0 && lane == 0) NTL(3, T);  // first batch's math done
           // before overwriting: Pᵀ is read by dV of the previous tile; this tile's dSᵀ buffer
           // (T & 1) by tile T-2's dQ MMA
           if (T >= 1) mbar_wait(bar_mm, (T - 1) & 1);
           if (T >= 2) mbar_wait(bar_dq + 8 * ds, ((T - 2) >> 1) & 1);
           tc_fence_after();
+          if (w == 0 && lane == 0) NTL(4, T);  // Pᵀ slot / dSᵀ buffer free
         }
         // Pᵀ -> TMEM (16 packed columns for these 32 queries); dSᵀ rows -> smem block qloc / 32
         tmem_st16(tP + lane_base + qloc / 2, pk);
@@ -427,12 +451,20 @@ __global__ void __launch_bounds__(512, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_ps);
+      if (w == 0 && lane == 0) NTL(5, T);  // hand-off
     }
   }
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
 }
+
+#ifdef EVO_TIMELINE
+extern "C" int evo_debug_nb_timeline_copy(void* dst, size_t bytes) {
+  if (bytes > sizeof(g_tlnb)) bytes = sizeof(g_tlnb);
+  return (int)cudaMemcpyFromSymbol(dst, g_tlnb, bytes);
+}
+#endif
 
 template <int DP>
 static cudaError_t launch_bwd_nb_t(const BwdFusedLaunch& L, cudaStream_t st) {

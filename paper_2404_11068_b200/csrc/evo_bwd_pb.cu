@@ -89,14 +89,24 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t bar_kvdone = smem_u32(&bars[16]);   // a batch row's last dV/dK MMA landed
   const uint32_t bar_dkvfree = smem_u32(&bars[17]);  // the drain warps pulled a row's dK/dV
   const uint32_t bar_bias = smem_u32(&bars[18]);     // the bias tiles of the prologue landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[19]);
+  // dq_pair (+8: buffer 1): the peer's half of a dQ tile landed in this CTA's receive buffer
+  // (the 2 keeping warps' expect-tx arrivals + the peer's st.async bytes) / the peer released its
+  // receive buffer (2 remote arrivals)
+  const uint32_t bar_recv = smem_u32(&bars[19]);
+  const uint32_t bar_recvfree = smem_u32(&bars[21]);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[23]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
   const int Lq_pad = nq * 128, Lk_pad = nk * 128;
-  const int c = (int)blockIdx.x % a.nchunks;
-  const int grp = (int)blockIdx.x / a.nchunks;
-  const int kt = grp % nk, h = grp / nk;
+  // dq_pair: the cluster's two CTAs are key tiles 0 and 1 of one (h, chunk); otherwise the grid
+  // is (h, key tile, chunk) with the chunk fastest
+  const bool pair = a.dq_pair != 0;
+  const int rank = pair ? (int)cluster_ctarank() : 0;
+  const int cid = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
+  const int c = cid % a.nchunks;
+  const int grp = cid / a.nchunks;
+  const int kt = pair ? rank : grp % nk, h = pair ? grp : grp / nk;
   const int k0 = kt * 128;
   const int b0 = c * a.chunk;
   const int nb = min(a.B - b0, a.chunk);
@@ -122,10 +132,15 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(bar_kvdone, 1);
     mbar_init(bar_dkvfree, 4);
     mbar_init(bar_bias, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_recv + 8 * i, 2);
+      mbar_init(bar_recvfree + 8 * i, 2);
+    }
     fence_barrier_init();
   }
   tc_fence_before();
-  __syncthreads();
+  if (pair) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tSig = tmem, tS = tmem + 256, tdP = tmem + 320, tP = tmem + 384;
@@ -264,6 +279,11 @@ __global__ void __launch_bounds__(512, 1)
                      pack_bf16(__uint_as_float(r[6]) * mul, __uint_as_float(r[7]) * mul));
       }
     };
+    constexpr uint32_t kHalfRows = 32 * DP * 4;  // bytes of one warp's 32 fp32 dQ rows
+    if (pair && (qd >> 1) == rank && lane == 0) {  // the first two receive phases (tiles 0, 1)
+      mbar_arrive_expect_tx(bar_recv, kHalfRows);
+      mbar_arrive_expect_tx(bar_recv + 8, kHalfRows);
+    }
     for (int T = 0; T < NT; ++T) {
       const int bi = T / nq, t = T - bi * nq;
       if (t == nq - 1) {  // the batch row's dK/dV, once its last dV/dK MMA landed
@@ -284,6 +304,72 @@ __global__ void __launch_bounds__(512, 1)
           tma_store_4d(&tm_dv, s0 + C::oStV + slice * kRbB, 0, k0 + (int)slice, h, b0 + bi);
           bulk_commit_group();
         }
+      }
+      if (pair) {
+        // dQ of tile T = dQ_0 + dQ_1 over the cluster, split by query halves: rank 0 stores
+        // queries 0-63 of the tile, rank 1 queries 64-127.  The drain warps of the other half
+        // send their fp32 rows into the peer's receive buffer (double-buffered by T & 1, 64 rows,
+        // swizzled like the fp32 staging); the keeping warps add the peer's rows to their own in
+        // the fixed order dQ_0 + dQ_1, scale, and store bf16 in place from the receive buffer.
+        mbar_wait(bar_dq + 8 * (T & 1), (T >> 1) & 1);
+        tc_fence_after();
+        uint32_t r[DP];
+        if constexpr (DP == 16) tmem_ld16(tdQ + lane_base, r);
+        else tmem_ld32(tdQ + lane_base, r);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_dqfree);  // the next tile's dQ MMA may overwrite TMEM
+        if (lane == 0 && qd == 0) PTL(13, 2 * T + 1);  // drain: own dQ pulled (qd 0)
+        if (lane == 0 && qd == 2) PTL(12, 2 * T + 1);  // drain: own dQ pulled (qd 2)
+        const int buf = T & 1;
+        const int hrow = (qd & 1) * 32 + lane;  // row within the 64-query half
+        const uint32_t rbuf = s0 + C::oStQ + buf * (64 * DP * 4);
+        if ((qd >> 1) != rank) {  // the peer keeps these rows: send them
+          if (T >= 2) mbar_wait_cluster(bar_recvfree + 8 * buf, ((T - 2) >> 1) & 1);
+          const uint32_t dst = mapa_shared(rbuf, (uint32_t)(rank ^ 1));
+          const uint32_t rbar = mapa_shared(bar_recv + 8 * buf, (uint32_t)(rank ^ 1));
+#pragma unroll
+          for (int i = 0; i < DP / 4; ++i)
+            st_async_v4(dst + swz_offset(hrow, i, DP * 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                        r[4 * i + 3], rbar);
+        } else {
+          mbar_wait_cluster(bar_recv + 8 * buf, (T >> 1) & 1);
+          uint32_t pk[DP / 2];
+#pragma unroll
+          for (int i = 0; i < DP / 4; ++i) {
+            const uint4 o = ld_shared_v4(rbuf + swz_offset(hrow, i, DP * 4));
+            const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+            // own + peer in key-tile order (rank 0's dQ first)
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const float m0 = __uint_as_float(r[4 * i + e]), p0 = __uint_as_float(ov[e]);
+              const float m1 = __uint_as_float(r[4 * i + e + 1]), p1 = __uint_as_float(ov[e + 1]);
+              const float s0f = (rank == 0 ? m0 + p0 : p0 + m0) * a.scale;
+              const float s1f = (rank == 0 ? m1 + p1 : p1 + m1) * a.scale;
+              pk[2 * i + e / 2] = pack_bf16(s0f, s1f);
+            }
+          }
+          // the receive rows are in registers: arm the buffer's next phase (tile T + 2) and
+          // release the buffer to the peer right away
+          __syncwarp();
+          if (lane == 0) {
+            if (T + 2 < NT) mbar_arrive_expect_tx(bar_recv + 8 * buf, kHalfRows);
+            mbar_arrive_remote(mapa_shared(bar_recvfree + 8 * buf, (uint32_t)(rank ^ 1)));
+          }
+          // this thread's query row of dq, bf16, straight to global memory (16-B stores)
+          const int q = t * 128 + qd * 32 + lane;
+          if (q < a.Lq) {
+            __nv_bfloat16* dqr = a.dq + (int64_t)(b0 + bi) * a.q_sb + (int64_t)h * a.q_sh + (int64_t)q * a.q_sl;
+#pragma unroll
+            for (int i = 0; i < DP / 8; ++i)  // D % 8 == 0 and 16-B aligned rows (use_dq_pair)
+              if (8 * i < a.D)
+                *reinterpret_cast<uint4*>(dqr + 8 * i) = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        }
+        if (lane == 0 && qd == 0) PTL(11, 2 * T + 1);  // drain: exchange done (qd 0)
+        if (lane == 0 && qd == 2) PTL(10, 2 * T);      // drain: exchange done (qd 2)
+        continue;
       }
       // dQ of tile T: bf16 rows with one key tile, else this key tile's fp32 part (reduce-add
       // into the one accumulator at nk == 2, its own part otherwise)
@@ -494,7 +580,8 @@ __global__ void __launch_bounds__(512, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (pair) cluster_sync_all();  // no CTA exits while its peer may still store / arrive into it
+  else __syncthreads();
   if (w == 0) tmem_dealloc<512>(tmem);
 }
 
@@ -514,8 +601,22 @@ static cudaError_t launch_bwd_pb_t(const BwdFusedLaunch& L, cudaStream_t st) {
   const int nk = (L.args.Lk + 127) / 128;
   const long long grid = (long long)L.args.H * nk * L.args.nchunks;
   if (grid == 0) return cudaSuccess;
-  kern<<<(unsigned)grid, 512, smem, st>>>(L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk,
-                                          L.tm_dv, L.tm_b, L.args);
+  if (L.args.dq_pair && nk != 2) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = L.args.dq_pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, L.tm_q, L.tm_k, L.tm_v, L.tm_da, L.tm_dq, L.tm_dk, L.tm_dv,
+                         L.tm_b, L.args);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -375,6 +375,13 @@ EVO_DEV void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, ui
                "r"(c), "r"(d)
                : "memory");
 }
+// asynchronous 16-B store into another CTA's shared memory whose completion (16 bytes of tx)
+// is signalled on that CTA's mbarrier (both addresses shared::cluster, from mapa_shared)
+EVO_DEV void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::
+                   "r"(addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
 // arrive (release at cluster scope) on an mbarrier of another CTA of the cluster
 EVO_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)

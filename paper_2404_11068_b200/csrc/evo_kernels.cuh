@@ -150,6 +150,9 @@ struct BwdFusedArgs {
   int kloop;       // no-bias kernel: 1 = each CTA walks every key tile of its (b, h) rows and
                    // accumulates dQ of all query tiles in TMEM (bf16 dQ, no fp32 parts);
                    // 0 = one key tile per CTA (grid H x nk x chunks)
+  int dq_pair;     // pair-bias kernel, exactly two key tiles: the two key tiles of a (h, chunk)
+                   // run as a 2-CTA cluster; rank 1 sends its fp32 dQ tile through distributed
+                   // shared memory and rank 0 stores dq = scale·(dQ_0 + dQ_1) in bf16
 };
 struct BwdFusedLaunch {
   CUtensorMap tm_q, tm_k, tm_v, tm_da, tm_b;

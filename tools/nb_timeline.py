@@ -85,6 +85,20 @@ for kind in sys.argv[1:] or ["col"]:
     if last:
         lx = np.array(last)
         print(f"  drain: dV/dK issued -> landed {med(tl[10][lx] - tl[8][lx]):.0f}")
+    if bias:
+        t1 = buf[1].astype(np.int64)
+        J1 = int(np.max(np.nonzero(t1[5])[0])) + 1
+        print(f"  CTA 1: {(t1[5][J1 - 1] - t1[5][0]) / (J1 - 1):.0f} per hand-off")
+        od = np.arange(1, J, 2)
+        for nm, tt in (("CTA 0", tl), ("CTA 1", t1)):
+            print(f"  {nm} drain per tile: dQ issued -> pulled qd0 {med(tt[13][od] - tt[9][od]):.0f} "
+                  f"qd2 {med(tt[12][od] - tt[9][od]):.0f}; pulled -> exchange done qd0 "
+                  f"{med(tt[11][od] - tt[13][od]):.0f} (max {np.max(tt[11][od] - tt[13][od])}) qd2 "
+                  f"{med(tt[10][od - 1] - tt[12][od]):.0f} (max {np.max(tt[10][od - 1] - tt[12][od])})")
+        if False:
+            print(f"  dQ drain (pair): dQ issued -> rank 1 data in {med(tl[13][od] - tl[9][od]):.0f}"
+                  f" -> stored {med(tl[11][od] - tl[13][od]):.0f}; rank 1 recvfree wait "
+                  f"{med(t1[11][od] - t1[9][od]):.0f} after its dQ issue")
     print("  first tiles (cycles from the first load): load S-ready S-issued wait landed b0 free "
           "handoff seen dkvfree dVdK dQ")
     for x in range(min(10, J)):
