@@ -75,6 +75,19 @@ def load():
     return _lib
 
 
+def _nvtx(name):
+    """NVTX range around a DAP phase or exchange (shows up in nsys / ncu timelines; a no-op
+    context without CUDA, e.g. in the gloo tests)."""
+    import contextlib
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.nvtx.range(name)
+    except Exception:
+        pass
+    return contextlib.nullcontext()
+
+
 def _check(rc):
     if rc != 0:
         from .evoattn import EvoError
@@ -167,8 +180,9 @@ class NcclDap:
         dst = out if out is not None else torch.empty(shape, dtype=src.dtype, device=src.device)
         nst = int(load().evo_dap_a2a_staging_bytes(self.h, A, Bd, C_bytes))
         st = self._stage(nst)
-        _check(load().evo_dap_alltoall_transpose(self.h, _p(src), _p(dst), _p(st), nst, A, Bd,
-                                                 C_bytes, direction, _stream(stream)))
+        with _nvtx(f"dap.transpose.dir{direction}"):
+            _check(load().evo_dap_alltoall_transpose(self.h, _p(src), _p(dst), _p(st), nst, A, Bd,
+                                                     C_bytes, direction, _stream(stream)))
         return dst
 
     def allgather(self, src, out=None, stream=None):
@@ -177,8 +191,9 @@ class NcclDap:
             raise ValueError("allgather: src must be contiguous")
         dst = out if out is not None else torch.empty((src.shape[0] * self.n,) + tuple(src.shape[1:]),
                                                       dtype=src.dtype, device=src.device)
-        _check(load().evo_dap_allgather(self.h, _p(src), _p(dst),
-                                        src.numel() * src.element_size(), _stream(stream)))
+        with _nvtx("dap.allgather"):
+            _check(load().evo_dap_allgather(self.h, _p(src), _p(dst),
+                                            src.numel() * src.element_size(), _stream(stream)))
         return dst
 
     def reduce_scatter(self, src, out=None, stream=None):
@@ -187,8 +202,9 @@ class NcclDap:
             raise ValueError("reduce_scatter: src must be contiguous fp32")
         dst = out if out is not None else torch.empty((src.shape[0] // self.n,) + tuple(src.shape[1:]),
                                                       dtype=src.dtype, device=src.device)
-        _check(load().evo_dap_reduce_scatter_f32(self.h, _p(src), _p(dst), dst.numel(),
-                                                 _stream(stream)))
+        with _nvtx("dap.reduce_scatter"):
+            _check(load().evo_dap_reduce_scatter_f32(self.h, _p(src), _p(dst), dst.numel(),
+                                                     _stream(stream)))
         return dst
 
     def barrier(self, stream=None):
@@ -272,8 +288,16 @@ class DapEvoformerAttention:
         x, c = self.x, self.comm
         s = {}
         cz, ctx, join = self._fork()
-        with ctx:
+        with ctx, _nvtx("dap.fwd.pair_stack"):
             z_next = self._forward_pair(x, cz, s)
+        with _nvtx("dap.fwd.msa_stack"):
+            self._forward_msa(x, c, s)
+        join(z_next, s["o_st"], s["o_end"])
+        self.saved = s
+        return s.pop("m_next"), z_next, {"o_row": s.pop("o_row"), "o_col": s.pop("o_col"),
+                                         "o_start": s["o_st"], "o_end": s["o_end"]}
+
+    def _forward_msa(self, x, c, s):
         # MSA stack: bias AG -> row attention -> a2a (S -> R) -> column attention -> a2a back
         s["E_row"] = c.allgather(x["E_row"])
         o_row, o_row_v, s["lse_row"] = M.attention_fwd("row", x["row_q"], x["row_k"], x["row_v"],
@@ -285,11 +309,8 @@ class DapEvoformerAttention:
         o_col, s["o_col_v"], s["lse_col"] = M.attention_fwd("col", s["col_q"], x["col_k"], x["col_v"],
                                                             x["col_g"], None, x["mask_col"],
                                                             self.attn)
-        m_next = c.transpose(o_col.reshape(o_col.shape[0], o_col.shape[1], Hm * D), 1)
-        join(z_next, s["o_st"], s["o_end"])
-        self.saved = s
-        return m_next, z_next, {"o_row": o_row, "o_col": o_col, "o_start": s["o_st"],
-                                "o_end": s["o_end"]}
+        s["m_next"] = c.transpose(o_col.reshape(o_col.shape[0], o_col.shape[1], Hm * D), 1)
+        s["o_row"], s["o_col"] = o_row, o_col
 
     def _forward_pair(self, x, c, s):
         # pair stack: bias AG -> triangle start -> a2a (I -> J) -> triangle end -> a2a back
@@ -311,9 +332,10 @@ class DapEvoformerAttention:
         x, c, s = self.x, self.comm, self.saved
         g = {}
         cz, ctx, join = self._fork()
-        with ctx:
+        with ctx, _nvtx("dap.bwd.pair_stack"):
             self._backward_pair(x, cz, s, g, dz_next)
-        self._backward_msa(x, c, s, g, dm_next)
+        with _nvtx("dap.bwd.msa_stack"):
+            self._backward_msa(x, c, s, g, dm_next)
         join(*g.values())
         return g
 

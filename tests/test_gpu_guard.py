@@ -4,8 +4,9 @@ output of the forward and backward is a strided VIEW inside a larger storage —
 after, all pre-filled with a sentinel bit pattern.  After the call every byte outside the views
 must still hold the sentinel and every element inside must have been written (no sentinel
 left), for ragged shapes that hit each kernel variant (fwd_occ with no / k-contiguous /
-q-contiguous bias, bwd_fused at nk = 1, 2 and >= 3, the two-pass backward, the fp32
-verification path) and for the workspace (its tail guard)."""
+q-contiguous bias; the pair-bias backward at nk = 1 and with the 2-CTA dQ pair sum at D = 16
+and 32; the no-bias backward at nk = 1, with fp32 parts, and with the in-CTA key-tile loop; the
+two-pass backward; the fp32 verification path) and for the workspace (its tail guard)."""
 import ctypes
 
 import numpy as np
@@ -70,6 +71,8 @@ CASES = [  # B, H, L, D, bias, bias_t, layout, dtype
     (2, 2, 96, 32, "batch", False, "blhd", torch.bfloat16),     # per-batch bias
     (3, 2, 100, 32, "shared", False, "blhd", torch.float32),    # fp32 verification mode
     (4, 2, 1, 32, "shared", False, "blhd", torch.bfloat16),     # L = 1
+    (3, 2, 250, 16, "shared", False, "blhd", torch.bfloat16),   # 2-CTA dQ pair sum at D = 16
+    (40, 4, 300, 32, None, False, "lbhd", torch.bfloat16),      # no-bias key-tile loop (B·H >= SMs)
 ]
 
 
