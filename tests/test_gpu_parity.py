@@ -58,6 +58,20 @@ def test_unequal_lengths():
     _assert(errs, torch.bfloat16)
 
 
+@pytest.mark.parametrize("B,H,Lq,Lk,D,bias_t,gate,layout", [
+    (6, 3, 256, 140, 16, True, False, "lbhd"),
+    (5, 2, 129, 256, 32, False, True, "blhd"),
+    (7, 4, 256, 256, 32, True, True, "bhld"),
+])
+def test_bf16_parity_dq_pair_sum(B, H, Lq, Lk, D, bias_t, gate, layout):
+    """A shared bias with two key tiles and Lq <= 256: the two key tiles of a head run as a
+    2-CTA cluster that sums dQ on chip (each keeps one 64-query half of every tile, the peer's
+    rows arrive by st.async); ragged key and query tiles, D = 16 and 32, gate on and off."""
+    errs, _, _ = run_case(B, H, Lq, Lk, D, seed=17, bias="shared", bias_t=bias_t, gate=gate,
+                          mask="prefix_fm", mask_t=layout == "lbhd", layout=layout)
+    _assert(errs, torch.bfloat16, f"dq pair B={B} H={H} Lq={Lq} Lk={Lk} D={D}")
+
+
 def test_seeds_cfg1_shape():
     for seed in range(5):
         errs, _, _ = run_case(32, 2, 32, 32, 16, seed=seed, bias="shared", mask="prefix_fm")
