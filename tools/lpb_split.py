@@ -3,6 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import torch
 from paper_2404_11068_b200 import evoattn
+if "--lib" in sys.argv:  # A/B against another build of the library
+    evoattn._LIB_PATH = os.path.abspath(sys.argv[sys.argv.index("--lib") + 1])
 dev = torch.device("cuda:0")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for rows, C, N in [(32768, 256, 1024), (65536, 128, 512), (262144, 64, 256)]:
