@@ -6,7 +6,8 @@
 using namespace evo;
 
 // MODE 0: same A/B every MMA; 1: A and B rotate over 8 tiles (K-major SW64); 2: rotate, B MN-major;
-// 3: TS (A from TMEM), B rotates MN-major; 4: rotate A K-major SW128 128-B rows (the Sᵀ form)
+// 3: TS (A from TMEM), B rotates MN-major; 4: rotate A K-major SW128 128-B rows (the Sᵀ form);
+// 5: rotate, A AND B MN-major (the backward's dQ = dS·K: A read from the dSᵀ blocks)
 template <int N, int MODE, int NACC = 2>
 __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -26,14 +27,16 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int n_mma) 
   tc_fence_after();
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
-    constexpr uint32_t idesc = make_idesc_bf16(128, N, 0, (MODE == 2 || MODE == 3) ? 1 : 0);
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, MODE == 5 ? 1 : 0, (MODE == 2 || MODE == 3 || MODE == 5) ? 1 : 0);
     unsigned long long t0 = clock64();
     for (int i = 0; i < n_mma; ++i) {
       const int r = MODE == 0 ? 0 : (i & 7);
       const uint32_t abase = s0 + r * 16384, bbase = s0 + 131072 + r * 8192;
-      const uint64_t ad = MODE == 4 ? make_sdesc(abase, 16, 1024, kSw128) : make_sdesc(abase, 16, 512, kSw64);
-      const uint64_t bd = (MODE == 2 || MODE == 3) ? make_sdesc(bbase, 8192, 512, kSw64)
-                                                   : make_sdesc(bbase, 16, 512, kSw64);
+      const uint64_t ad = MODE == 4 ? make_sdesc(abase, 16, 1024, kSw128)
+                          : MODE == 5 ? make_sdesc(abase, 8192, 512, kSw64)
+                                      : make_sdesc(abase, 16, 512, kSw64);
+      const uint64_t bd = (MODE == 2 || MODE == 3 || MODE == 5) ? make_sdesc(bbase, 8192, 512, kSw64)
+                                                                : make_sdesc(bbase, 16, 512, kSw64);
       const uint32_t d = tm + (uint32_t)((i % NACC) * N);
       if (MODE == 3) umma_bf16_ts(d, tm + 256 + (i & 7) * 8, bd, idesc, 1);
       else umma_bf16(d, ad, bd, idesc, 1);
@@ -82,5 +85,7 @@ int main() {
   run<128, 1>("SS fresh tiles");
   run<256, 1>("SS fresh tiles");
   run<128, 0>("SS same tiles");
+  run<32, 5, 1>("SS fresh A+B MN-major (dQ), ONE acc");
+  run<32, 5>("SS fresh A+B MN-major (dQ)");
   return 0;
 }
