@@ -580,11 +580,10 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
     fa.t0 = 0;
     fa.sigma_only = 0;
     if ((e = traced(st, "bwd_fused", [&] {
-           // bias, Lq <= 256: 64-query hand-offs; 256 < Lq <= 384: the Σ-split kernel; no bias:
-           // 128-query hand-offs
+           // bias: 64-query hand-offs (256 < Lq <= 384: Σ of the first 256 queries, the Σ-only
+           // pass below adds the last tile's); no bias: 128-query hand-offs
            return !bm ? evo::launch_bwd_nb_bf16(F, dpad(d->D), st)
-                      : big ? evo::launch_bwd_fused_bf16(F, dpad(d->D), 1, st)
-                            : evo::launch_bwd_pb_bf16(F, dpad(d->D), st);
+                      : evo::launch_bwd_pb_bf16(F, dpad(d->D), st);
          })) != cudaSuccess)
       return cuda_fail(e, "bwd_fused");
     if (big) {

@@ -1,7 +1,8 @@
 // evo_bwd_fused.cu — single-pass bf16 backward on sm_100a: dK, dV, dQ and the pair-bias
 // gradient of one (head, 128-key tile) for a chunk of batch rows, in one persistent CTA.
-// Shipped for a shared bias with 256 < Lq <= 384 only (the BIG instantiation, BASELINE cfg 5):
-// Lq <= 256 with a bias runs on evo_bwd_pb.cu and no bias on evo_bwd_nb.cu.
+// Shipped only as the Σ-only pass (sigma_only, first query tile 2) of a shared bias with
+// 256 < Lq <= 384 (BASELINE cfg 5): the gradients and the first 256 queries' Σ run on
+// evo_bwd_pb.cu (BIG), no bias on evo_bwd_nb.cu.
 //
 // Same arithmetic as evo_bwd.cu's bwd_main + bwd_bias (SPEC.md L168
 // recompute backward; dbias = Σ_b dS over the broadcast axis, PAPER.md L294 / north star), but
@@ -627,8 +628,8 @@ extern "C" int evo_debug_timeline_copy(void* dst, size_t bytes) {
 }
 #endif
 
-// Only the BIG instantiation ships: Lq <= 256 with a bias runs on evo_bwd_pb.cu, no bias on
-// evo_bwd_nb.cu (both faster)
+// Only the BIG instantiation ships, as the Σ-only pass of 256 < Lq <= 384 with a bias (the main
+// pass is evo_bwd_pb.cu's BIG variant; no bias runs on evo_bwd_nb.cu — DESIGN §7c)
 cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st) {
   const bool big = has_bias && ((L.args.Lq + 127) / 128) * 128 > 256;
   if (!big) return cudaErrorInvalidValue;

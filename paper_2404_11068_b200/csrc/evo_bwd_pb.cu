@@ -43,15 +43,18 @@ __device__ unsigned long long g_tlpb[2][16][512];
 #define PTL(ev, i) do { } while (0)
 #endif
 
-template <int DP>
+// BIG: a shared bias with 256 < Lq <= 384 (BASELINE cfg 5, N_res = 384): the resident biasᵀ grows
+// to [128 k][384 q] and the dSᵀ tile buffer is single (smem 226 KB); Σ_b dSᵀ stays in TMEM for the
+// first 256 queries and the last query tile's Σ comes from the Σ-only pass of evo_bwd_fused.cu
+template <int DP, bool BIG = false>
 struct PbCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
   static constexpr uint32_t kTile = 128 * kRowBytes;  // one 128-row Q/K/V/dA tile
-  static constexpr uint32_t oBias = 0;                 // [128 k][256 q] bf16, 4 x [128][64] SW128
-  static constexpr uint32_t oKV = oBias + 65536;       // stage s: K at +s*2*kTile, V +kTile
+  static constexpr uint32_t oBias = 0;  // [128 k][256 | 384 q] bf16, 4 | 6 x [128][64] SW128
+  static constexpr uint32_t oKV = oBias + (BIG ? 98304 : 65536);  // stage s: K +s*2*kTile, V +kTile
   static constexpr uint32_t oQA = oKV + 4 * kTile;     // stage s: Q at +s*2*kTile, dA +kTile
-  static constexpr uint32_t oDS = oQA + 4 * kTile;     // 2 x 4 x [128 k][32 q] SW64 (8 KB)
-  static constexpr uint32_t oVec = oDS + 65536;        // 2 x (lse2[128], D[128]) fp32
+  static constexpr uint32_t oDS = oQA + 4 * kTile;     // (2 | 1) x 4 x [128 k][32 q] SW64 (8 KB)
+  static constexpr uint32_t oVec = oDS + (BIG ? 32768 : 65536);  // 2 x (lse2[128], D[128]) fp32
   static constexpr uint32_t oStK = oVec + 2048;        // staging: dK, dV bf16, dQ bf16|fp32
   static constexpr uint32_t oStV = oStK + kTile;
   static constexpr uint32_t oStQ = oStV + kTile;
@@ -59,14 +62,14 @@ struct PbCfg {
   static constexpr uint32_t kSmem = oBar + 256;
 };
 
-template <int DP>
+template <int DP, bool BIG>
 __global__ void __launch_bounds__(512, 1)
     bwd_pb_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_da,
                   const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
                   const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_b,
                   const BwdFusedArgs a) {
-  using C = PbCfg<DP>;
+  using C = PbCfg<DP, BIG>;
   static_assert(DP == 16 || DP == 32, "pair-bias backward: head dim pad 16 or 32");
   static_assert(C::kSmem <= 232448, "pair-bias backward: shared memory");
   constexpr uint32_t kSw = DP == 32 ? kSw64 : kSw32;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_after();
         const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
         const uint32_t ab = qb + C::kTile;
-        const uint32_t db = s0 + C::oDS + ds * 32768;
+        const uint32_t db = s0 + C::oDS + (BIG ? 0 : ds) * 32768;
         // dV += Pᵀ·dA (K = the hand-off's 64 queries; A = Pᵀ from TMEM): K steps 0,1 read the
         // Pᵀ columns of query half 0, steps 2,3 of half 1 — one commit each, so each half of the
         // next hand-off may overwrite its columns as soon as they are consumed
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(512, 1)
           umma_bf16(tdQ, make_sdesc(db + kk * 1024, 8192, 512, kSw64),
                     make_sdesc(kb + kk * 16 * C::kRowBytes, 16384, 8 * C::kRowBytes, kSw),
                     idesc_q, kk > 0 ? 1u : 0u);
-        umma_commit(bar_dq + 8 * ds);
+        umma_commit(bar_dq + 8 * (BIG ? 0 : ds));
         PTL(9, j);  // dQ issued
         // every reader of the Q/dA stage (Sᵀ/dPᵀ MMAs: pulled before the hand-off; dV/dK/dQ:
         // this thread) and, after a row's last tile, of the K/V stage is done once these land
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(512, 1)
         // send their fp32 rows into the peer's receive buffer (double-buffered by T & 1, 64 rows,
         // swizzled like the fp32 staging); the keeping warps add the peer's rows to their own in
         // the fixed order dQ_0 + dQ_1, scale, and store bf16 in place from the receive buffer.
-        mbar_wait(bar_dq + 8 * (T & 1), (T >> 1) & 1);
+        if (BIG) mbar_wait(bar_dq, T & 1);
+        else mbar_wait(bar_dq + 8 * (T & 1), (T >> 1) & 1);
         tc_fence_after();
         uint32_t r[DP];
         if constexpr (DP == 16) tmem_ld16(tdQ + lane_base, r);
@@ -373,7 +377,8 @@ __global__ void __launch_bounds__(512, 1)
       }
       // dQ of tile T: bf16 rows with one key tile, else this key tile's fp32 part (reduce-add
       // into the one accumulator at nk == 2, its own part otherwise)
-      mbar_wait(bar_dq + 8 * (T & 1), (T >> 1) & 1);
+      if (BIG) mbar_wait(bar_dq, T & 1);
+      else mbar_wait(bar_dq + 8 * (T & 1), (T >> 1) & 1);
       tc_fence_after();
       if (lane == 0) bulk_wait_group_read0();
       __syncwarp();
@@ -426,20 +431,34 @@ __global__ void __launch_bounds__(512, 1)
         mbar_arrive_expect_tx(bar_bias, (uint32_t)(Lq_pad / 64) * 16384u);
         for (int sg = 0; sg < Lq_pad / 64; ++sg)
           tma_load_4d(sBias + sg * 16384, &tm_b, bar_bias, sg * 64, k0, h, 0);
-      } else {
+      } else if (!BIG) {
         mbar_arrive_expect_tx(bar_bias, 65536u);  // two [256 q][64 k] boxes (zero-filled past Lq)
         tma_load_4d(s0 + C::oDS, &tm_b, bar_bias, k0, 0, h, 0);
         tma_load_4d(s0 + C::oDS + 32768, &tm_b, bar_bias, k0 + 64, 0, h, 0);
       }
     }
-    mbar_wait(bar_bias, 0);
-    if (a.bmode != 2) {
-      const int nq8 = Lq_pad / 8;  // 8-query blocks
+    if (a.bmode == 2 || !BIG) mbar_wait(bar_bias, 0);
+    // k-contiguous: one pass over all queries ([256 q][64 k] x 2 staged), or for BIG passes of
+    // 128 queries ([128 q][64 k] x 2 = the single 32 KB dSᵀ buffer)
+    const int npass = a.bmode != 2 ? (BIG ? Lq_pad / 128 : 1) : 0;
+    for (int ps = 0; ps < npass; ++ps) {
+      const int qb0 = BIG ? ps * 128 : 0;                // first query of the pass
+      const int nq8 = BIG ? 16 : Lq_pad / 8;            // 8-query blocks in the pass
+      const uint32_t kbox = BIG ? 16384u : 32768u;      // staged [q][64 k] box bytes
+      if (BIG) {
+        if (tid == 0) {
+          mbar_arrive_expect_tx(bar_bias, 32768u);
+          tma_load_4d(s0 + C::oDS, &tm_b, bar_bias, k0, qb0, h, 0);
+          tma_load_4d(s0 + C::oDS + 16384, &tm_b, bar_bias, k0 + 64, qb0, h, 0);
+        }
+        mbar_wait(bar_bias, ps & 1);
+      }
       const int mi = lane >> 3, ri = lane & 7;
       for (int gi = w; gi < nq8 * 4; gi += 8) {  // x4 group: q block q8, k blocks 4 kk..4 kk+3
-        const int q8 = gi >> 2, k8 = (gi & 3) * 4 + mi;
-        const uint32_t ql = (uint32_t)(q8 * 8 + ri);
-        const uint32_t src = s0 + C::oDS + (uint32_t)(k8 >> 3) * 32768u + ql * 128u +
+        const int q8l = gi >> 2, k8 = (gi & 3) * 4 + mi;
+        const int q8 = qb0 / 8 + q8l;
+        const uint32_t ql = (uint32_t)(q8l * 8 + ri);
+        const uint32_t src = s0 + C::oDS + (uint32_t)(k8 >> 3) * kbox + ql * 128u +
                              ((((uint32_t)k8 & 7u) ^ (ql & 7u)) << 4);
         uint32_t r0, r1, r2, r3;
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -452,6 +471,7 @@ __global__ void __launch_bounds__(512, 1)
                      "r"(r0), "r"(r1), "r"(r2), "r"(r3)
                      : "memory");
       }
+      if (BIG) named_bar_sync(1, 256);  // the staging is reloaded by the next pass
     }
     named_bar_sync(1, 256);  // the staging (dSᵀ buffers) is free and the resident bias complete
 
@@ -494,7 +514,8 @@ __global__ void __launch_bounds__(512, 1)
       tmem_ld32(tS + lane_base + hq * 32, rs);
       tmem_ld32(tdP + lane_base + hq * 32, rd);
       // Σ_b dSᵀ so far for these 32 columns (this thread's lane, last written a batch row ago)
-      if (bi > 0) tmem_ld32(tSig + lane_base + qcol, acc);
+      const bool do_sig = !BIG || t < 2;  // BIG: the last query tile's Σ is the Σ-only pass's
+      if (do_sig && bi > 0) tmem_ld32(tSig + lane_base + qcol, acc);
       tmem_wait_ld();
       if (w == 0 && lane == 0) PTL(14, j);  // Sᵀ/dPᵀ/Σ in registers
       tc_fence_before();
@@ -544,18 +565,22 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
       if (w == 0 && lane == 0) PTL(15, j);  // math done
-      tmem_st32(tSig + lane_base + qcol, acc);
+      if (do_sig) tmem_st32(tSig + lane_base + qcol, acc);
       // before overwriting: this half's Pᵀ columns are read by dV of the previous hand-off; the
       // tile's dSᵀ buffer (T & 1) by tile T-2's dQ MMA
       if (w == 0 && lane == 0) PTL(3, j);  // math + Σ done
       if (j >= 1) mbar_wait(hq ? bar_mm1 : bar_mm0, (j - 1) & 1);
-      if (s == 0 && T >= 2) mbar_wait(bar_dq + 8 * ds, ((T - 2) >> 1) & 1);
+      if (BIG) {  // single dSᵀ buffer: tile T-1's dQ MMA must have read it
+        if (s == 0 && T >= 1) mbar_wait(bar_dq, (T - 1) & 1);
+      } else if (s == 0 && T >= 2) {
+        mbar_wait(bar_dq + 8 * ds, ((T - 2) >> 1) & 1);
+      }
       tc_fence_after();
       if (w == 0 && lane == 0) PTL(4, j);  // Pᵀ columns / dSᵀ buffer free
       // Pᵀ -> TMEM (16 packed columns for these 32 queries); dSᵀ rows -> smem block qt / 32
       tmem_st16(tP + lane_base + hq * 16, pk);
       {
-        const uint32_t db = s0 + C::oDS + ds * 32768 + (qt >> 5) * 8192;
+        const uint32_t db = s0 + C::oDS + (BIG ? 0 : ds) * 32768 + (qt >> 5) * 8192;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           st_shared_v4(db + pd_off[e], dk2[4 * e], dk2[4 * e + 1], dk2[4 * e + 2], dk2[4 * e + 3]);
@@ -571,7 +596,7 @@ __global__ void __launch_bounds__(512, 1)
     // ---- Σ_b dSᵀ of the chunk -> partial[c][h][q][k0 + row]: warp half hq writes the 32-query
     // column blocks hq, hq + 2, ...
     float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
-    for (int cbk = hq; cbk < nq * 4; cbk += 2) {
+    for (int cbk = hq; cbk < (BIG ? 2 : nq) * 4; cbk += 2) {
       uint32_t acc[32];
       tmem_ld32(tSig + lane_base + cbk * 32, acc);
       tmem_wait_ld();
@@ -592,10 +617,10 @@ extern "C" int evo_debug_pb_timeline_copy(void* dst, size_t bytes) {
 }
 #endif
 
-template <int DP>
+template <int DP, bool BIG>
 static cudaError_t launch_bwd_pb_t(const BwdFusedLaunch& L, cudaStream_t st) {
-  auto kern = bwd_pb_kernel<DP>;
-  const size_t smem = PbCfg<DP>::kSmem;
+  auto kern = bwd_pb_kernel<DP, BIG>;
+  const size_t smem = PbCfg<DP, BIG>::kSmem;
   cudaError_t e = set_smem_once(kern, smem);
   if (e != cudaSuccess) return e;
   const int nk = (L.args.Lk + 127) / 128;
@@ -621,8 +646,10 @@ static cudaError_t launch_bwd_pb_t(const BwdFusedLaunch& L, cudaStream_t st) {
 }
 
 cudaError_t launch_bwd_pb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st) {
-  if (DP == 16) return launch_bwd_pb_t<16>(L, st);
-  if (DP == 32) return launch_bwd_pb_t<32>(L, st);
+  const bool big = ((L.args.Lq + 127) / 128) * 128 > 256;
+  if (big && L.args.dq_pair) return cudaErrorInvalidValue;
+  if (DP == 16) return big ? launch_bwd_pb_t<16, true>(L, st) : launch_bwd_pb_t<16, false>(L, st);
+  if (DP == 32) return big ? launch_bwd_pb_t<32, true>(L, st) : launch_bwd_pb_t<32, false>(L, st);
   return cudaErrorInvalidValue;
 }
 
