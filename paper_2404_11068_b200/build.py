@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", INC, "-I", CSRC]
 
-ATTN_SRCS = ["evo_api.cu", "evo_fwd_occ.cu", "evo_bwd.cu", "evo_bwd_fused.cu", "evo_bwd_nb.cu", "evo_bwd_pb.cu",
+ATTN_SRCS = ["evo_api.cu", "evo_fwd_occ.cu", "evo_bwd.cu", "evo_bwd_nb.cu", "evo_bwd_pb.cu",
              "evo_f32.cu",
              "evo_pair_bias.cu",
              "evo_global_attn.cu", "evo_ln_proj.cu"]

@@ -157,7 +157,8 @@ struct WsLayout {
   int nchunks = 1, chunk = 1;
   bool fused = false;
 };
-// Single-pass backward (evo_bwd_fused.cu) for bf16 with a shared bias or none and Lq <= 256
+// Single-pass backward (evo_bwd_pb.cu / evo_bwd_nb.cu) for bf16 with a shared bias (Lq <= 384)
+// or none
 bool use_fused_bwd(const evo_attn_desc_t* d) {
   if (d->dtype != EVO_BF16 || d->bias_kind == EVO_BIAS_PER_BATCH) return false;
   const int Lq_pad = ((d->Lq + 127) / 128) * 128;
@@ -590,7 +591,7 @@ evo_status_t evo_attn_bwd(const evo_attn_desc_t* d, const void* q, const void* k
       ++nl;
       fa.t0 = 2;
       fa.sigma_only = 1;
-      if ((e = traced(st, "bwd_fused_sigma", [&] { return evo::launch_bwd_fused_bf16(F, dpad(d->D), 1, st); })) != cudaSuccess) return cuda_fail(e, "bwd_fused (sigma pass)");
+      if ((e = traced(st, "bwd_fused_sigma", [&] { return evo::launch_bwd_pb_bf16(F, dpad(d->D), st); })) != cudaSuccess) return cuda_fail(e, "bwd_pb (sigma pass)");
     }
     ++nl;
     // fork: the dbias reduce runs on the side stream while dq_convert runs on the caller's

@@ -3,7 +3,7 @@
 // (head, 128-key tile) for a chunk of batch rows, in one persistent CTA, one 128 x 128 (key x
 // query) block per hand-off.
 //
-// Same arithmetic as evo_bwd_fused.cu (P recomputed once from lse,
+// Same arithmetic as evo_bwd_pb.cu (P recomputed once from lse,
 // dS = P ⊙ (dP − D), dV = Pᵀ dA, dK = scale dSᵀ Q, dQ = scale dS K), but without
 // the Σ_b dSᵀ accumulator the tensor memory has room for a whole query tile: Sᵀ and dPᵀ are
 // single N = 128 MMAs (one per K step) and the compute warps hand a full 128-query tile to the

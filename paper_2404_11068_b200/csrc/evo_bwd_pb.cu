@@ -1,14 +1,15 @@
-// evo_bwd_pb.cu — single-pass bf16 backward WITH a shared pair bias, Lq <= 256 (MSA row
+// evo_bwd_pb.cu — single-pass bf16 backward WITH a shared pair bias, Lq <= 384 (MSA row
 // attention with pair bias, triangle attention around the starting / ending node: BASELINE
-// cfg 1-3 and the block's three bias modules) on sm_100a: dK, dV, dQ and Σ_b dSᵀ (the pair-bias
-// gradient) of one (head, 128-key tile) for a chunk of batch rows, in one persistent CTA.
+// cfg 1-3 and 5 and the block's three bias modules) on sm_100a: dK, dV, dQ and Σ_b dSᵀ (the
+// pair-bias gradient) of one (head, 128-key tile) for a chunk of batch rows, in one persistent
+// CTA.
 //
-// Same arithmetic as evo_bwd_fused.cu (P recomputed once from lse,
+// The backward of the pair-bias attention (P recomputed once from lse,
 // dS = P ⊙ (dP − D), dV = Pᵀ dA, dK = scale dSᵀ Q, dQ = scale dS K, dbias = Σ_b dS over the
 // broadcast axis), with the hand-off structure of the no-bias kernel
 // (evo_bwd_nb.cu): 64-query hand-offs (N = 64 Sᵀ/dPᵀ MMAs, two per 128-query tile) processed by
-// all eight compute warps at once instead of the ping-pong groups of 32-query sub-tiles, whose
-// mbarrier round trips under-fed the tensor pipe.  Σ_b dSᵀ of the key tile stays in
+// all eight compute warps at once (round 2 replaced a design with two ping-pong warpgroups on
+// 32-query sub-tiles, whose mbarrier round trips under-fed the tensor pipe).  Σ_b dSᵀ of the key tile stays in
 // TMEM (fp32, read-modify-write by the owning thread), 256 columns; that leaves room for exactly
 // one 64-query Sᵀ/dPᵀ slot, one Pᵀ slot and dV/dK/dQ.
 //
@@ -45,7 +46,8 @@ __device__ unsigned long long g_tlpb[2][16][512];
 
 // BIG: a shared bias with 256 < Lq <= 384 (BASELINE cfg 5, N_res = 384): the resident biasᵀ grows
 // to [128 k][384 q] and the dSᵀ tile buffer is single (smem 226 KB); Σ_b dSᵀ stays in TMEM for the
-// first 256 queries and the last query tile's Σ comes from the Σ-only pass of evo_bwd_fused.cu
+// first 256 queries and the last query tile's Σ comes from a second, Σ-only launch of this kernel
+// (sigma_only, first query tile t0 = 2: Sᵀ/dPᵀ MMAs and the compute warps only)
 template <int DP, bool BIG = false>
 struct PbCfg {
   static constexpr uint32_t kRowBytes = DP * 2;
@@ -100,8 +102,12 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(&bars[23]);
 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int nq = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
-  const int Lq_pad = nq * 128, Lk_pad = nk * 128;
+  const int nq_all = (a.Lq + 127) >> 7, nk = (a.Lk + 127) >> 7;
+  const int Lq_pad = nq_all * 128, Lk_pad = nk * 128;
+  // query tiles t0 .. nq_all-1 (t0 = 2 in the Σ-only pass of a BIG call: Σ_b dSᵀ of the last
+  // query tile, no gradients); every loop runs t over [0, nq) with query tile t0 + t
+  const int t0 = a.t0, nq = nq_all - t0;
+  const bool sig_only = a.sigma_only != 0;
   // dq_pair: the cluster's two CTAs are key tiles 0 and 1 of one (h, chunk); otherwise the grid
   // is (h, key tile, chunk) with the chunk fastest
   const bool pair = a.dq_pair != 0;
@@ -123,7 +129,9 @@ __global__ void __launch_bounds__(512, 1)
       mbar_init(bar_kv + 8 * i, 1);
       mbar_init(bar_in + 8 * i, 1);
       mbar_init(bar_kvfree + 8 * i, 1);
-      mbar_init(bar_infree + 8 * i, 1);
+      // the Σ-only pass frees a Q/dA/vector stage when the 8 compute warps are done with the
+      // tile's lse2/D vectors (the gradient issuer's dQ commit does it otherwise)
+      mbar_init(bar_infree + 8 * i, sig_only ? 8 : 1);
       mbar_init(bar_dq + 8 * i, 1);
     }
     mbar_init(bar_sp, 1);
@@ -172,9 +180,9 @@ __global__ void __launch_bounds__(512, 1)
           const uint32_t qb = s0 + C::oQA + st * 2 * C::kTile;
           const uint32_t bar = bar_in + 8 * st;
           mbar_arrive_expect_tx(bar, 2 * C::kTile + 1024);
-          tma_load_4d(qb, &tm_q, bar, 0, t * 128, h, b);
-          tma_load_4d(qb + C::kTile, &tm_da, bar, 0, t * 128, h, b);
-          const int64_t vrow = ((int64_t)b * a.H + h) * Lq_pad + t * 128;
+          tma_load_4d(qb, &tm_q, bar, 0, (t0 + t) * 128, h, b);
+          tma_load_4d(qb + C::kTile, &tm_da, bar, 0, (t0 + t) * 128, h, b);
+          const int64_t vrow = ((int64_t)b * a.H + h) * Lq_pad + (t0 + t) * 128;
           bulk_load(s0 + C::oVec + st * 1024, a.lse2 + vrow, 512, bar);
           bulk_load(s0 + C::oVec + st * 1024 + 512, a.Dvec + vrow, 512, bar);
         }
@@ -203,11 +211,13 @@ __global__ void __launch_bounds__(512, 1)
                     make_sdesc(qb + C::kTile + kk * 32, 16, 8 * C::kRowBytes, kSw), idesc_s, kk > 0);
         umma_commit(bar_sp);
         PTL(0, j);  // Sᵀ/dPᵀ issued
+        if (sig_only && s == 1 && t == nq - 1)  // no gradient MMAs in the Σ-only pass: the
+          umma_commit(bar_kvfree + 8 * kvs);    // Sᵀ/dPᵀ MMAs are K/V's last readers
       }
     }
   } else if (w == 10) {
     // ------------------------------------------------------------------ gradient-MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && !sig_only) {
       constexpr uint32_t idesc_kv = make_idesc_bf16(128, DP, 0, 1);  // dV, dK (B MN-major)
       constexpr uint32_t idesc_q = make_idesc_bf16(128, DP, 1, 1);   // dQ (A, B MN-major)
       for (int j = 0; j < J; ++j) {
@@ -262,7 +272,7 @@ __global__ void __launch_bounds__(512, 1)
         if (t == nq - 1) umma_commit(bar_kvfree + 8 * kvs);
       }
     }
-  } else if (w >= 12) {
+  } else if (w >= 12 && !sig_only) {
     // ------------------------------------------------------------------ drain warps
     const int qd = w & 3;
     const int row = qd * 32 + lane;  // TMEM lane: a key row (dK/dV) or a query row (dQ)
@@ -505,7 +515,8 @@ __global__ void __launch_bounds__(512, 1)
         keep = (keep_word >> (bi & 31)) & 1u;
       }
       const int qt = s * 64 + hq * 32;  // this warp's first query within the tile
-      const int qcol = t * 128 + qt;    // ... within the padded query range (= its Σ column)
+      const int qcol = t * 128 + qt;    // its Σ column (query tiles relative to t0)
+      const int qabs = (t0 + t) * 128 + qt;  // ... and its query in the padded range
       if (w == 0 && lane == 0) PTL(1, j);  // waits for Sᵀ/dPᵀ
       mbar_wait(bar_sp, j & 1);
       tc_fence_after();
@@ -514,7 +525,8 @@ __global__ void __launch_bounds__(512, 1)
       tmem_ld32(tS + lane_base + hq * 32, rs);
       tmem_ld32(tdP + lane_base + hq * 32, rd);
       // Σ_b dSᵀ so far for these 32 columns (this thread's lane, last written a batch row ago)
-      const bool do_sig = !BIG || t < 2;  // BIG: the last query tile's Σ is the Σ-only pass's
+      // BIG main pass: the last query tile's Σ is the Σ-only pass's
+      const bool do_sig = !BIG || sig_only || t < 2;
       if (do_sig && bi > 0) tmem_ld32(tSig + lane_base + qcol, acc);
       tmem_wait_ld();
       if (w == 0 && lane == 0) PTL(14, j);  // Sᵀ/dPᵀ/Σ in registers
@@ -532,7 +544,7 @@ __global__ void __launch_bounds__(512, 1)
         const uint4 d0 = ld_shared_v4(vbase + 512 + gq * 32), d1 = ld_shared_v4(vbase + 512 + gq * 32 + 16);
         const uint32_t nl[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
         const uint32_t nd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-        const uint32_t cq = (uint32_t)(qcol >> 3) + gq;  // 8-query chunk of the resident biasᵀ
+        const uint32_t cq = (uint32_t)(qabs >> 3) + gq;  // 8-query chunk of the resident biasᵀ
         const uint4 bv = ld_shared_v4(sBias + (cq >> 3) * 16384u + row * 128u + (((cq & 7u) ^ (row & 7u)) << 4));
         const uint32_t bu[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
@@ -566,6 +578,14 @@ __global__ void __launch_bounds__(512, 1)
       }
       if (w == 0 && lane == 0) PTL(15, j);  // math done
       if (do_sig) tmem_st32(tSig + lane_base + qcol, acc);
+      if (sig_only) {  // Σ-only pass: no Pᵀ/dSᵀ hand-off, no gradient MMAs, no drains
+        if (s == 1) {  // this warp's last read of the tile's lse2/D: the stage may be reloaded
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_infree + 8 * st);
+        }
+        if (s == 1 && ++t == nq) { t = 0; ++bi; }
+        continue;
+      }
       // before overwriting: this half's Pᵀ columns are read by dV of the previous hand-off; the
       // tile's dSᵀ buffer (T & 1) by tile T-2's dQ MMA
       if (w == 0 && lane == 0) PTL(3, j);  // math + Σ done
@@ -595,8 +615,10 @@ __global__ void __launch_bounds__(512, 1)
     }
     // ---- Σ_b dSᵀ of the chunk -> partial[c][h][q][k0 + row]: warp half hq writes the 32-query
     // column blocks hq, hq + 2, ...
-    float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row;
-    for (int cbk = hq; cbk < (BIG ? 2 : nq) * 4; cbk += 2) {
+    float* dst = a.partial + ((int64_t)c * a.H + h) * Lq_pad * (int64_t)Lk_pad + k0 + row +
+                 (int64_t)t0 * 128 * Lk_pad;
+    const int sig_tiles = (BIG && !sig_only) ? 2 : nq;
+    for (int cbk = hq; cbk < sig_tiles * 4; cbk += 2) {
       uint32_t acc[32];
       tmem_ld32(tSig + lane_base + cbk * 32, acc);
       tmem_wait_ld();

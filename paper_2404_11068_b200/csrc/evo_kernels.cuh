@@ -118,7 +118,8 @@ inline size_t bwd_bias_smem_bytes(int DP) {
 }
 cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
-// Fused backward (evo_bwd_fused.cu): CTA per (h, 128-key tile, batch chunk); dK, dV, dQ parts
+// Single-pass backward (evo_bwd_pb.cu with a bias, evo_bwd_nb.cu without): CTA per (h, 128-key
+// tile, batch chunk); dK, dV, dQ
 // and the chunk's dbias partial in one pass (shared bias or none; Lq <= 256).
 struct BwdFusedArgs {
   int B, H, Lq, Lk, D;
@@ -175,7 +176,6 @@ inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
   *chunk = ch;
   return (B + ch - 1) / ch;
 }
-cudaError_t launch_bwd_fused_bf16(const BwdFusedLaunch& L, int DP, int has_bias, cudaStream_t st);
 // the no-bias backward (evo_bwd_nb.cu): same launch block and workspace, one 128-query tile per
 // hand-off (N = 128 Sᵀ/dPᵀ MMAs); DP 16 or 32
 cudaError_t launch_bwd_nb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);

@@ -1,4 +1,4 @@
-// Throughput of the fused backward's per-element math (evo_bwd_fused.cu compute loop) on register
+// Throughput of the backward's per-element math (the evo_bwd_pb.cu / round-1 fused kernel compute loop) on register
 // data, 16 warps per SM (4 per sub-partition), in variants that drop one part at a time:
 //   0 full:    x = bias·log2e - lse2 (FFMA2), x += S·scale·log2e (FFMA2), p = ex2 x2, dS = p·(dP - D)
 //              (FADD2, FMUL2), Σ += dS (FADD2), pack p and dS to bf16x2 (2 F2FP)
