@@ -118,9 +118,8 @@ inline size_t bwd_bias_smem_bytes(int DP) {
 }
 cudaError_t launch_bwd_bias_bf16(const BwdBiasLaunch& L, int DP, int bias_mode, cudaStream_t st);
 
-// Single-pass backward (evo_bwd_pb.cu with a bias, evo_bwd_nb.cu without): CTA per (h, 128-key
-// tile, batch chunk); dK, dV, dQ
-// and the chunk's dbias partial in one pass (shared bias or none; Lq <= 256).
+// Single-pass backward (evo_bwd_pb.cu with a shared bias, Lq <= 384; evo_bwd_nb.cu without):
+// CTA per (h, 128-key tile, batch chunk); dK, dV, dQ and the chunk's dbias partial in one pass.
 struct BwdFusedArgs {
   int B, H, Lq, Lk, D;
   float scale, scale_log2;
@@ -179,8 +178,9 @@ inline int bwd_fused_nchunks(int B, int H, int nk, int num_sms, int* chunk) {
 // the no-bias backward (evo_bwd_nb.cu): same launch block and workspace, one 128-query tile per
 // hand-off (N = 128 Sᵀ/dPᵀ MMAs); DP 16 or 32
 cudaError_t launch_bwd_nb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
-// the pair-bias kernel (evo_bwd_pb.cu) for a shared bias with Lq <= 256: 64-query hand-offs
-// processed by all eight compute warps, Σ_b dSᵀ in TMEM; DP 16 or 32
+// the pair-bias kernel (evo_bwd_pb.cu) for a shared bias, Lq <= 384 (above 256: the BIG variant,
+// then a Σ-only launch with t0 = 2, sigma_only = 1): 64-query hand-offs processed by all eight
+// compute warps, Σ_b dSᵀ in TMEM; DP 16 or 32
 cudaError_t launch_bwd_pb_bf16(const BwdFusedLaunch& L, int DP, cudaStream_t st);
 // the key-tile loop of the no-bias kernel keeps nq dQ accumulators (DP columns each) in TMEM
 // next to Sᵀ, dPᵀ, Pᵀ (320 columns), dV and dK
